@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""rGSVD benchmark: pairs/s and sketch-GEMM TFLOP/s on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config cfg1] [--impl reference]
+
+A step is one full randomized GSVD + comparative analysis of one matrix
+pair (BASELINE.json configs; cfg1 by default: fp64, m=20000, p=16000,
+n=1000, k=60, q=2) with a fresh Ω seed per step (the reference's
+run_bench convention, bench.py:98-102). Synthetic seeded data with the
+config's shape/rank/noise (paper_2404_09459_b200/workloads.py) stands in
+for the paper's genome datasets.
+
+value  : pairs/s with G1, G2 resident in HBM (whole job = all ranks).
+e2e    : the same through the public API with G1, G2 in pinned HOST
+         memory: every step copies them H2D and reads the report D2H.
+roofline: the dominant GEMM kernel timed live with CUDA events on its
+         stream; algorithmic flops 2 m n k per launch; peak = FP64 DMMA
+         issue peak measured on this pool (profiles/r01_fp64_peak.log).
+cpu_baseline: the CPU oracle (numpy restatement of the reference with the
+         q power iterations; OpenBLAS on the host cores) on a bounded sample.
+N > 1 : one process per GPU, each rank an independent replica pair (the
+         pairs are independent), timed as the max over ranks ("weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_DMMA_PEAK_TFLOPS = 37.0  # tools/fp64_peak.cu on this pool's B200 (profiles/r01_fp64_peak.log)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, r[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, budget_s: float, g1, g2):
+    """Oracle restatement on the host cores, bounded sample of whole pairs."""
+    from oracle import rgsv_oracle as orc
+
+    t_start = time.perf_counter()
+    done = 0
+    while True:
+        orc.run_pipeline(g1, g2, k=cfg.k, q=cfg.q, seed=done)
+        done += 1
+        if time.perf_counter() - t_start > budget_s or done >= 50:
+            break
+    dt = time.perf_counter() - t_start
+    return {"value": done / dt, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{done} whole {cfg.name} pairs (k={cfg.k}, q={cfg.q}) through "
+                      f"oracle/rgsv_oracle.run_pipeline, numpy {__import__('numpy').__version__}"
+                      f" + OpenBLAS on {os.cpu_count()} host threads, {dt:.1f} s"}
+
+
+def workload_desc(cfg):
+    return (f"{cfg.name}: {cfg.dtype} rGSVD pair m={cfg.m} p={cfg.p} n={cfg.n} s={cfg.s} "
+            f"(shared {cfg.shared}) decay 10^(-{cfg.decay:g} j/s) eps={cfg.eps:g} k={cfg.k} "
+            f"q={cfg.q}, fixed-rank range finder, Omega seed = step index")
+
+
+def run_reference(args, rank, world):
+    from paper_2404_09459_b200.workloads import CONFIGS, make_pair
+
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    g1, g2 = make_pair(cfg)
+    from oracle import rgsv_oracle as orc
+
+    for i in range(args.warmup):
+        orc.run_pipeline(g1, g2, k=cfg.k, q=cfg.q, seed=i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        orc.run_pipeline(g1, g2, k=cfg.k, q=cfg.q, seed=i)
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    line = {
+        "impl": "reference", "metric": f"rGSVD pairs/sec ({cfg.name})", "value": value,
+        "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg), "parallelism": "host cores"},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": f"{args.steps} whole pairs through the numpy restatement of "
+                                   "the reference (oracle/rgsv_oracle.py; the reference has no "
+                                   "power iteration, SURVEY.md §0 F1)"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_kernel(fn, reps=20):
+    import torch
+
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e-3
+
+
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_09459_b200 as rg
+    from paper_2404_09459_b200 import _native
+    from paper_2404_09459_b200 import device as dv
+    from paper_2404_09459_b200.engine import run_device_pipeline
+    from paper_2404_09459_b200.workloads import CONFIGS, make_pair
+
+    cfg = CONFIGS[args.config]
+    g1h, g2h = make_pair(cfg, data_seed=cfg.data_seed + rank)
+    g1 = torch.from_numpy(g1h).cuda()
+    g2 = torch.from_numpy(g2h).cuda()
+    pair = rg.GmpPair.resident(g1, g2)
+
+    def opts(seed):
+        return rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(cfg.k, seed, cfg.q))
+
+    for i in range(args.warmup):
+        run_device_pipeline(pair, opts(i))
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident throughput
+    barrier()
+    clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
+    l0 = _native.lib().rgsv_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        run_device_pipeline(pair, opts(i))
+    e1.record(stream)
+    barrier()
+    launches = _native.lib().rgsv_launch_count() - l0
+    t = e0.elapsed_time(e1) * 1e-3
+    clk = clocks.stop() if clocks else None
+    tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max = float(tt.item())
+    value = args.steps * world / t_max
+
+    # ---- end to end through the public API from pinned host memory
+    g1p = torch.from_numpy(g1h).pin_memory()
+    g2p = torch.from_numpy(g2h).pin_memory()
+    plan = dv.pair_plan(cfg.m, cfg.p, cfg.n, cfg.k, cfg.k)
+
+    def e2e_step(i):
+        d1 = g1p.to("cuda", non_blocking=True)
+        d2 = g2p.to("cuda", non_blocking=True)
+        return rg.compare(rg.GmpPair.resident(d1, d2), opts(i))
+
+    for i in range(min(2, args.warmup)):
+        e2e_step(i)
+    barrier()
+    e0.record(stream)
+    for i in range(args.steps):
+        rep = e2e_step(i)
+    e1.record(stream)
+    barrier()
+    te = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = args.steps * world / float(te.item())
+    h2d = (g1h.nbytes + g2h.nbytes + plan.s1.om_dev.numel() * 8 + plan.s2.om_dev.numel() * 8)
+    d2h = plan.pk.nbytes
+
+    # ---- dominant kernel, timed live (CUDA events on its stream)
+    L = _native.lib()
+    kp = dv.ceil16(cfg.k)
+    ldb = dv.ceil16(cfg.n)
+    Q = torch.randn(cfg.m, kp, dtype=torch.float64, device="cuda")
+    Q[:, cfg.k:] = 0
+    Bo = torch.zeros(kp, ldb, dtype=torch.float64, device="cuda")
+    Xt = torch.zeros(kp, ldb, dtype=torch.float64, device="cuda")
+    Xt[: cfg.k, : cfg.n] = torch.randn(cfg.k, cfg.n, dtype=torch.float64, device="cuda")
+    Y = torch.zeros(cfg.m, kp, dtype=torch.float64, device="cuda")
+    scratch = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    st = dv.sp(stream)
+    gmat = pair.g1
+
+    def gtq():
+        L.rgsv_gemm_gtq(dv.vp(Q), kp, dv.vp(gmat.t), gmat.ld, dv.vp(Bo), ldb, kp, cfg.n, cfg.m,
+                        dv.vp(scratch), scratch.numel(), st)
+
+    def gx():
+        L.rgsv_gemm_gx(dv.vp(gmat.t), gmat.ld, dv.vp(Xt), ldb, dv.vp(Y), kp, cfg.m, kp, cfg.n,
+                       dv.vp(scratch), scratch.numel(), st)
+
+    t_gtq = time_kernel(gtq)
+    t_gx = time_kernel(gx)
+    flop = 2.0 * cfg.m * cfg.n * cfg.k
+    per_pair = (cfg.q + 1)  # launches of each shape per matrix
+    dom_name, dom_t = ("gemm_gtq (B = Q^T G, DMMA)", t_gtq) if t_gtq >= t_gx else \
+        ("gemm_gx (Y = G X, DMMA)", t_gx)
+    achieved = flop / dom_t / 1e12
+    # sketch-GEMM TFLOP/s over all 2q+2 passes of both matrices, from the
+    # per-launch times scaled by each matrix's rows
+    gemm_time = per_pair * (t_gtq + t_gx) * (cfg.m + cfg.p) / cfg.m
+    sketch_tflops = cfg.flops / gemm_time / 1e12
+    step_s = t_max / args.steps
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_gtq_cfg1_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world >= 1:
+        cpu = cpu_baseline(cfg, args.cpu_sample_seconds, g1h, g2h)
+
+    if rank == 0:
+        line = {
+            "metric": f"rGSVD pairs/sec ({cfg.name}); sketch-GEMM TFLOP/s (% FP64 TC roofline)",
+            "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(cfg),
+                       "g_bytes": cfg.g_bytes,
+                       "l2": "inputs larger than L2 (G1+G2 = %.0f MB > 126 MB)" % (cfg.g_bytes / 1e6),
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved,
+                         "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,
+                         "flop_per_launch": flop, "launch_us": dom_t * 1e6,
+                         "peak_source": "measured FP64 DMMA issue peak (tools/fp64_peak.cu; "
+                                        "MEASURED_PEAKS.json has no FP64 figure)",
+                         "share_of_step": per_pair * 2 * dom_t * (cfg.m + cfg.p) / cfg.m / step_s},
+            "sketch_gemm_tflops": sketch_tflops,
+            "sketch_gemm_frac_of_peak": sketch_tflops / FP64_DMMA_PEAK_TFLOPS,
+            "kernel_us": {"gemm_gtq": t_gtq * 1e6, "gemm_gx": t_gx * 1e6},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "path": "paper_2404_09459_b200.compare() with G in pinned host memory"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "check": {"r": int(rep.spectrum.r), "s": int(rep.spectrum.s), "d1": rep.d1,
+                      "d2": rep.d2},
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

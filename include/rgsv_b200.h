@@ -1,0 +1,139 @@
+/*
+ * rgsv_b200 — C-ABI of the B200 (sm_100a) randomized-GSVD hot path.
+ *
+ * This is the drop-in boundary for the reference package rgsv 0.1.0, whose
+ * hot path is pure Python over numpy/LAPACK and therefore has no FFI of its
+ * own. Each entry point below replaces one reference
+ * stage; the citation names the reference code it stands in for
+ * (paths under /root/reference/pkg/src/rgsv/). The Python host layer
+ * (paper_2404_09459_b200/, loaded with ctypes) rebuilds the reference's
+ * dataclasses around these calls; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - All matrices are row-major FP64 in DEVICE memory; ld* are row strides
+ *     in elements and must be even (TMA needs 16-byte row pitch).
+ *   - kp = k rounded up to a multiple of 16; padded rows/columns are zero
+ *     on output and must be zero on input.
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     asynchronous on it. Return codes report argument/launch errors;
+ *     numerical failures detected on the device are OR-ed into the caller's
+ *     device `status` word (RGSV_ST_* bits) and read back with the results.
+ *   - Results are bitwise deterministic for fixed inputs (fixed-order
+ *     reductions, no floating-point atomics).
+ */
+#ifndef RGSV_B200_H
+#define RGSV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes, mapped 1:1 onto the reference exceptions (errors.py:5-56) */
+#define RGSV_OK 0
+#define RGSV_ERR_DIMENSION 1   /* DimensionError */
+#define RGSV_ERR_VALIDATION 2  /* ValidationError */
+#define RGSV_ERR_RANK 3        /* RankDeficiencyError */
+#define RGSV_ERR_CONVERGENCE 4 /* ConvergenceError */
+#define RGSV_ERR_CUDA 5        /* launch/driver failure (RuntimeError) */
+#define RGSV_ERR_WORKSPACE 6   /* workspace too small (internal) */
+#define RGSV_ERR_DEGENERATE 7  /* DegenerateSpectrumError */
+
+/* device status bits */
+#define RGSV_ST_CHOL_BREAKDOWN 0x1  /* nonpositive Cholesky pivot */
+#define RGSV_ST_NONFINITE 0x2       /* NaN/Inf in G (core.py:55) */
+#define RGSV_ST_JACOBI 0x4          /* Jacobi SVD did not converge (core.py:102-105) */
+#define RGSV_ST_CLASSIFY 0x8        /* overlapping zero classes (engine.py:179-180) */
+#define RGSV_ST_DEGENERATE 0x10     /* vanishing alpha/beta energy (analysis.py:58-59) */
+#define RGSV_ST_NOT_NORMALIZED 0x20 /* |sum p - 1| > 1e-10 (analysis.py:74-75) */
+
+const char* rgsv_version(void);
+
+/* Number of kernels this library has launched so far in the process
+ * (bench.py reports the delta over its timed region as gpu_launches). */
+long long rgsv_launch_count(void);
+
+/* Compute capability (major*10+minor) of the current device, or -1. */
+int rgsv_device_cc(void);
+
+/* --- (1)-(3) range finder + projection for ONE matrix -------------------
+ * Replaces rangefinder.extract_basis in fixed-rank mode (one block of
+ * width k: rangefinder.py:106-133 with blocksize = max_cols = k,
+ * trim_tol = 0) followed by q power iterations (not in the reference,
+ * SURVEY.md §0 F1) and the projection c = Q^H G (engine.py:255-256).
+ *   Y = G Omega; Q = qr(Y).q; q x { Qhat = qr(G^T Q).q; Q = qr(G Qhat).q };
+ *   B = Q^T G.
+ * Inputs : g (m x n, ldg), omega_t = Omega^T (kp x n, ld_omega; rows >= k zero).
+ * Outputs: q_out (m x kp, ld kp), b_out (kp x n, ldb),
+ *          stats[0] = ||G||_F^2 (rangefinder.py:83), stats[1] = ||B||_F^2
+ *          (the captured energy of rangefinder.py:123),
+ *          rdiag[k] = |diag R| of the final QR (the trim test, :120).
+ * QR is shifted CholeskyQR3 (R diagonal > 0: the core.py:88-95 phase
+ * convention). */
+size_t rgsv_sketch_workspace_bytes(int64_t m, int64_t n, int k);
+int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
+                        const double* omega_t, int64_t ld_omega, int k, int q, double* q_out,
+                        double* b_out, int64_t ldb, double* stats, double* rdiag, int* status,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* --- (4) small GSVD -------------------------------------------------------
+ * Replaces engine.py:257-261 (reduced_qr of vstack(c1, c2), L blocks) and
+ * engine._singular_values (engine.py:228-231) for the two L blocks:
+ * sv1 (min(l1, r) values, descending), sv2 (min(l2, r)), r = rank dim of
+ * the stacked QR = min(l1 + l2, n). nsv[0..1] receive the counts.
+ * One-sided Jacobi SVD; non-convergence sets RGSV_ST_JACOBI. */
+size_t rgsv_small_gsvd_workspace_bytes(int l1, int l2, int64_t n);
+int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, int64_t ldb2, int l2,
+                    int64_t n, double* sv1, double* sv2, int* nsv, int* status, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* --- (5) spectrum + comparative quantities -------------------------------
+ * Replaces engine.spectrum_from_l_blocks (engine.py:189-225, merged
+ * completion), classify_spectrum (engine.py:164-186) and analysis.py:37-79
+ * (rho, theta, P1, P2, D1, D2) in one kernel.
+ * counts[0] = r, counts[1] = s; scalars = {d1, d2, sum p1, sum p2}. */
+int rgsv_comparative(const double* sv1, const int* nsv, const double* sv2, int64_t n,
+                     double classify_tol, double* alphas, double* betas, double* rho,
+                     double* theta, double* p1, double* p2, double* scalars, int* counts,
+                     int* status, void* stream);
+
+/* Per-quantity forms of analysis.py:37-79 for a given spectrum (alphas,
+ * betas, r): rho (inf for i < r), theta, p1, p2, scalars = {d1, d2, sum p1,
+ * sum p2}; and D of a given probability vector (scalars[0] = D,
+ * scalars[2] = sum p). */
+int rgsv_spectrum_quantities(const double* alphas, const double* betas, int64_t n, int r,
+                             double* rho, double* theta, double* p1, double* p2, double* scalars,
+                             int* status, void* stream);
+int rgsv_entropy(const double* p, int64_t n, double* scalars, void* stream);
+
+/* Singular values (descending, min(rows, cols) of them) of a small dense
+ * matrix by one-sided Jacobi: core.svd values (core.py:99-106). nsv[0]
+ * receives the count; nsv[1] is scratch. */
+size_t rgsv_svd_values_workspace_bytes(int rows, int cols);
+int rgsv_svd_values(const double* a, int64_t lda, int rows, int cols, double* sv, int* nsv,
+                    int* status, void* workspace, size_t workspace_bytes, void* stream);
+
+/* --- building blocks (row-sharded multi-GPU driver, tests) ---------------
+ * gemm_gx : C (M x N) = A (M x K) * Bt^T, Bt given N x K.
+ * gemm_gtq: C (M x N) = A^T * B, A: K x M, B: K x N (reduction over rows).
+ * chol_inv: Cholesky of a k x k Gram (ld kp) [+ shift for `shift_rows`
+ *           rows], Linv = L^{-1}, Rinv = Linv^T (kp x kp, identity pad).
+ * sumsq   : out[0] = sum of squares of a rows x cols block. */
+int rgsv_gemm_gx(const double* a, int64_t lda, const double* bt, int64_t ldb, double* c,
+                 int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
+                 size_t scratch_bytes, void* stream);
+int rgsv_gemm_gtq(const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                  int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
+                  size_t scratch_bytes, void* stream);
+int rgsv_chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv,
+                  double* rinv, double* rdiag, int* status, void* stream);
+int rgsv_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
+               void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RGSV_B200_H */

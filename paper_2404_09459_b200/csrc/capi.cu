@@ -1,0 +1,474 @@
+// extern "C" boundary (include/rgsv_b200.h) and the native pipeline driver.
+#include <string.h>
+
+#include <atomic>
+
+#include "common.cuh"
+#include "rgsv_internal.h"
+
+namespace rgsv {
+
+// defined in small.cu
+int launch_stack(double* s, int64_t lds, const double* b1, int64_t ld1, int l1, const double* b2,
+                 int64_t ld2, int l2, int lp, int64_t n, cudaStream_t st);
+int launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
+                      int transpose, cudaStream_t st);
+int launch_jacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, double* v2,
+                  int64_t ld2, int nv2, int len2, double* sv2, int* nsv2, int* status,
+                  cudaStream_t st);
+int launch_comparative(const double* sv1, const int* nsv, const double* sv2, int64_t n, double tol,
+                       double* a, double* b, double* rho, double* theta, double* p1, double* p2,
+                       double* scalars, int* counts, int* status, int mode, int r_given,
+                       cudaStream_t st);
+int launch_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
+                 double* part, int max_parts, cudaStream_t st);
+int launch_sum(const double* part, int n, double* out, cudaStream_t st);
+
+static std::atomic<long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+
+int make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer,
+                 uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer, int elem_bytes) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return RGSV_ERR_CUDA;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld_elems * elem_bytes) & 15))
+    return RGSV_ERR_DIMENSION;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * (uint64_t)elem_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                  2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : RGSV_ERR_CUDA;
+}
+
+static inline int64_t ceil16(int64_t x) { return (x + 15) / 16 * 16; }
+static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Upper bound of split-K partial storage for the GEMMs of one pipeline.
+static size_t split_scratch_bytes(int64_t m, int64_t n, int64_t kp) {
+  const int64_t ldn = ceil16(n);
+  size_t a = (size_t)kSMs * kp * kp;                 // tall Gram partials
+  int64_t tiles = (n + 255) / 256;
+  if (tiles < 1) tiles = 1;
+  size_t b = (size_t)(kSMs / tiles + 1) * kp * ldn;  // gtq projection partials
+  size_t c = (size_t)kSMs * 128 * kp;                // gx tail partials
+  size_t d = (size_t)32 * kp * kp + (size_t)8 * kp * ldn;  // wide gram + wide TRSM
+  size_t mx = a;
+  if (b > mx) mx = b;
+  if (c > mx) mx = c;
+  if (d > mx) mx = d;
+  (void)m;
+  return mx * sizeof(double) + 4096;
+}
+
+struct SketchLayout {
+  size_t y, z, z2, gram, linv, rinv, rdiag, ss, tmp, scratch, total, scratch_bytes;
+};
+
+static SketchLayout sketch_layout(int64_t m, int64_t n, int k) {
+  const int64_t kp = ceil16(k), ldn = ceil16(n);
+  SketchLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = al256(off + bytes);
+    return o;
+  };
+  L.y = take((size_t)m * kp * 8);
+  L.z = take((size_t)kp * ldn * 8);
+  L.z2 = take((size_t)kp * ldn * 8);
+  L.gram = take((size_t)kp * kp * 8);
+  L.linv = take((size_t)kp * kp * 8 + (size_t)kp * (kp + 1) * 8);
+  L.rinv = take((size_t)kp * kp * 8);
+  L.rdiag = take((size_t)kp * 8);
+  L.ss = take(4096 * 8);
+  L.tmp = take(64 * 8);
+  L.scratch_bytes = split_scratch_bytes(m, n, kp);
+  L.scratch = take(L.scratch_bytes);
+  L.total = off;
+  return L;
+}
+
+}  // namespace rgsv
+
+using namespace rgsv;
+
+extern "C" {
+
+long long rgsv_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* rgsv_version(void) { return "rgsv_b200 0.1.0 (sm_100a, FP64 DMMA + TMA)"; }
+
+int rgsv_device_cc(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  int ma = 0, mi = 0;
+  if (cudaDeviceGetAttribute(&ma, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&mi, cudaDevAttrComputeCapabilityMinor, dev);
+  return ma * 10 + mi;
+}
+
+size_t rgsv_sketch_workspace_bytes(int64_t m, int64_t n, int k) {
+  return sketch_layout(m, n, k).total;
+}
+
+int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
+                        const double* omega_t, int64_t ld_omega, int k, int q, double* q_out,
+                        double* b_out, int64_t ldb, double* stats, double* rdiag, int* status,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (m < 1 || n < 1 || k < 1 || q < 0) return RGSV_ERR_DIMENSION;
+  if (k > m || k > n) return RGSV_ERR_VALIDATION;  // rangefinder.py:88-91
+  const int64_t kp = ceil16(k), ldn = ceil16(n);
+  if (kp > 512) return RGSV_ERR_DIMENSION;
+  if (ldg < n || ld_omega < n || ldb < n || (ldg & 1) || (ld_omega & 1) || (ldb & 1))
+    return RGSV_ERR_DIMENSION;
+  SketchLayout L = sketch_layout(m, n, k);
+  if (workspace_bytes < L.total) return RGSV_ERR_WORKSPACE;
+  char* ws = static_cast<char*>(workspace);
+  double* y = reinterpret_cast<double*>(ws + L.y);
+  double* z = reinterpret_cast<double*>(ws + L.z);
+  double* z2 = reinterpret_cast<double*>(ws + L.z2);
+  double* gram = reinterpret_cast<double*>(ws + L.gram);
+  double* linv = reinterpret_cast<double*>(ws + L.linv);
+  double* rinv = reinterpret_cast<double*>(ws + L.rinv);
+  double* rd_ws = reinterpret_cast<double*>(ws + L.rdiag);
+  double* ss = reinterpret_cast<double*>(ws + L.ss);
+  double* scratch = reinterpret_cast<double*>(ws + L.scratch);
+  const size_t sb = L.scratch_bytes;
+
+  // (1) sketch Y = G Omega, fused ||G||_F^2 (rangefinder.py:83,115)
+  GemmArgs s;
+  s.A = g;
+  s.lda = ldg;
+  s.B = omega_t;
+  s.ldb = ld_omega;
+  s.C = y;
+  s.ldc = kp;
+  s.M = m;
+  s.N = kp;
+  s.K = n;
+  s.scratch = scratch;
+  s.scratch_bytes = sb;
+  s.max_split = 32;
+  s.ss_out = ss;
+  int ss_units = 0;
+  s.ss_units = &ss_units;
+  if (int e = gemm_gx(s, st)) return e;
+  if (ss_units > 4096) return RGSV_ERR_WORKSPACE;
+  if (int e = launch_sum(ss, ss_units, stats, st)) return e;
+  // (2) Q = qr(Y).q  (rangefinder.py:119)
+  double* qres = nullptr;
+  if (int e = cholqr3_tall(y, q_out, m, k, (int)kp, gram, linv, rd_ws, scratch, sb, status, &qres,
+                           st))
+    return e;
+  for (int it = 0; it < q; ++it) {
+    // Z^T = Q^T G, Qhat = qr(Z).q, Y = G Qhat, Q = qr(Y).q
+    GemmArgs p;
+    p.A = q_out;
+    p.lda = kp;
+    p.B = g;
+    p.ldb = ldg;
+    p.C = z;
+    p.ldc = ldn;
+    p.M = kp;
+    p.N = n;
+    p.K = m;
+    p.scratch = scratch;
+    p.scratch_bytes = sb;
+    p.max_split = kSMs;
+    if (int e = gemm_gtq(p, st)) return e;
+    double* qt = nullptr;
+    if (int e = cholqr3_wide(z, z2, n, ldn, k, (int)kp, gram, linv, rinv, rd_ws, scratch, sb,
+                             status, &qt, st))
+      return e;
+    GemmArgs y2 = s;
+    y2.B = qt;
+    y2.ldb = ldn;
+    y2.ss_out = nullptr;
+    y2.ss_units = nullptr;
+    if (int e = gemm_gx(y2, st)) return e;
+    if (int e = cholqr3_tall(y, q_out, m, k, (int)kp, gram, linv, rd_ws, scratch, sb, status,
+                             &qres, st))
+      return e;
+  }
+  // (3) B = Q^T G (engine.py:255) and its energy (rangefinder.py:123)
+  GemmArgs p;
+  p.A = q_out;
+  p.lda = kp;
+  p.B = g;
+  p.ldb = ldg;
+  p.C = b_out;
+  p.ldc = ldb;
+  p.M = kp;
+  p.N = n;
+  p.K = m;
+  p.scratch = scratch;
+  p.scratch_bytes = sb;
+  p.max_split = kSMs;
+  if (int e = gemm_gtq(p, st)) return e;
+  if (int e = launch_sumsq(b_out, ldb, kp, n, stats + 1, ss, 1024, st)) return e;
+  if (rdiag) {
+    if (cudaMemcpyAsync(rdiag, rd_ws, k * sizeof(double), cudaMemcpyDeviceToDevice, st) !=
+        cudaSuccess)
+      return RGSV_ERR_CUDA;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- small GSVD
+namespace {
+struct SmallLayout {
+  size_t s, s2, t, t2, gram, linv, rinv, rdiag, v1, v2, scratch, total, scratch_bytes;
+  int64_t lp, lds, kpn;
+};
+SmallLayout small_layout(int l1, int l2, int64_t n) {
+  SmallLayout L{};
+  const int64_t l = l1 + l2;
+  L.lp = ceil16(l);
+  L.lds = ceil16(n);
+  L.kpn = ceil16(n);
+  const int64_t rows = L.lp > l ? L.lp : l;
+  const int64_t kmax = L.lp > L.kpn ? L.lp : L.kpn;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = al256(off + bytes);
+    return o;
+  };
+  L.s = take((size_t)rows * L.lds * 8);
+  L.s2 = take((size_t)rows * L.lds * 8);
+  L.t = take((size_t)L.lp * L.lp * 8);
+  L.t2 = take((size_t)L.lp * L.lp * 8);
+  L.gram = take((size_t)kmax * kmax * 8);
+  L.linv = take((size_t)kmax * kmax * 8 + (size_t)kmax * (kmax + 1) * 8);
+  L.rinv = take((size_t)kmax * kmax * 8);
+  L.rdiag = take((size_t)kmax * 8);
+  L.v1 = take((size_t)(l1 + 1) * (kmax + 1) * 8 + (size_t)l1 * l * 8);
+  L.v2 = take((size_t)(l2 + 1) * (kmax + 1) * 8 + (size_t)l2 * l * 8);
+  L.scratch_bytes = split_scratch_bytes(l, n, kmax) + (size_t)kSMs * kmax * kmax * 8;
+  L.scratch = take(L.scratch_bytes);
+  L.total = off;
+  return L;
+}
+}  // namespace
+
+size_t rgsv_small_gsvd_workspace_bytes(int l1, int l2, int64_t n) {
+  return small_layout(l1, l2, n).total;
+}
+
+int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, int64_t ldb2, int l2,
+                    int64_t n, double* sv1, double* sv2, int* nsv, int* status, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (l1 < 0 || l2 < 0 || n < 1) return RGSV_ERR_DIMENSION;
+  const int l = l1 + l2;
+  if (l == 0) return RGSV_ERR_RANK;  // engine.py:258-259
+  SmallLayout L = small_layout(l1, l2, n);
+  if (workspace_bytes < L.total) return RGSV_ERR_WORKSPACE;
+  char* ws = static_cast<char*>(workspace);
+  double* S = reinterpret_cast<double*>(ws + L.s);
+  double* S2 = reinterpret_cast<double*>(ws + L.s2);
+  double* T = reinterpret_cast<double*>(ws + L.t);
+  double* T2 = reinterpret_cast<double*>(ws + L.t2);
+  double* gram = reinterpret_cast<double*>(ws + L.gram);
+  double* linv = reinterpret_cast<double*>(ws + L.linv);
+  double* rinv = reinterpret_cast<double*>(ws + L.rinv);
+  double* rdiag = reinterpret_cast<double*>(ws + L.rdiag);
+  double* v1 = reinterpret_cast<double*>(ws + L.v1);
+  double* v2 = reinterpret_cast<double*>(ws + L.v2);
+  double* scratch = reinterpret_cast<double*>(ws + L.scratch);
+  const size_t sb = L.scratch_bytes;
+  const int64_t lp = L.lp, lds = L.lds;
+
+  double* Q = nullptr;
+  int64_t ldq = 0;
+  int r = 0;
+  if (l <= n) {
+    // S = [B1; B2] (l x n, wide). S^T = P T (CholQR3 on S^T), so
+    // range(S) = range(T^T) and the Q of qr(S) is the Q of qr(T^T).
+    if (int e = launch_stack(S, lds, b1, ldb1, l1, b2, ldb2, l2, (int)lp, n, st)) return e;
+    if (lp > 512) return RGSV_ERR_DIMENSION;
+    double* pt = nullptr;
+    if (int e = cholqr3_wide(S, S2, n, lds, l, (int)lp, gram, linv, rinv, rdiag, scratch, sb,
+                             status, &pt, st))
+      return e;
+    // T^T = S P  (lp x lp)
+    double* ssrc = (pt == S) ? S2 : S;  // the buffer not holding P^T was overwritten: rebuild S
+    if (int e = launch_stack(ssrc, lds, b1, ldb1, l1, b2, ldb2, l2, (int)lp, n, st)) return e;
+    GemmArgs tt;
+    tt.A = ssrc;
+    tt.lda = lds;
+    tt.B = pt;
+    tt.ldb = lds;
+    tt.C = T;
+    tt.ldc = lp;
+    tt.M = lp;
+    tt.N = lp;
+    tt.K = n;
+    tt.scratch = scratch;
+    tt.scratch_bytes = sb;
+    tt.max_split = 32;
+    if (int e = gemm_gx(tt, st)) return e;
+    if (int e = cholqr3_tall(T, T2, l, l, (int)lp, gram, linv, rdiag, scratch, sb, status, &Q,
+                             st))
+      return e;
+    ldq = lp;
+    r = l;
+  } else {
+    // tall stacked matrix (l > n): Q = qr(S).q directly
+    const int64_t kpn = L.kpn;
+    if (kpn > 512) return RGSV_ERR_DIMENSION;
+    if (int e = launch_stack(S, kpn, b1, ldb1, l1, b2, ldb2, l2, l, n, st)) return e;
+    if (int e = cholqr3_tall(S, S2, l, (int)n, (int)kpn, gram, linv, rdiag, scratch, sb, status,
+                             &Q, st))
+      return e;
+    ldq = kpn;
+    r = (int)n;
+  }
+  // L1 = Q[:l1, :r], L2 = Q[l1:, :r]; Jacobi on whichever side has fewer vectors
+  int nv1, len1, nv2, len2;
+  int64_t ld1, ld2;
+  if (l1 <= r) {
+    nv1 = l1; len1 = r; ld1 = r;
+    if (int e = launch_copy_block(v1, ld1, Q, ldq, l1, r, 0, st)) return e;
+  } else {
+    nv1 = r; len1 = l1; ld1 = l1;
+    if (int e = launch_copy_block(v1, ld1, Q, ldq, r, l1, 1, st)) return e;
+  }
+  if (l2 <= r) {
+    nv2 = l2; len2 = r; ld2 = r;
+    if (int e = launch_copy_block(v2, ld2, Q + (int64_t)l1 * ldq, ldq, l2, r, 0, st)) return e;
+  } else {
+    nv2 = r; len2 = l2; ld2 = l2;
+    if (int e = launch_copy_block(v2, ld2, Q + (int64_t)l1 * ldq, ldq, r, l2, 1, st)) return e;
+  }
+  return launch_jacobi(v1, ld1, nv1, len1, sv1, nsv, v2, ld2, nv2, len2, sv2, nsv + 1, status, st);
+}
+
+int rgsv_comparative(const double* sv1, const int* nsv, const double* sv2, int64_t n,
+                     double classify_tol, double* alphas, double* betas, double* rho,
+                     double* theta, double* p1, double* p2, double* scalars, int* counts,
+                     int* status, void* stream) {
+  if (n < 1) return RGSV_ERR_DIMENSION;
+  if (!(classify_tol > 0.0 && classify_tol < 1e-2)) return RGSV_ERR_VALIDATION;
+  return launch_comparative(sv1, nsv, sv2, n, classify_tol, alphas, betas, rho, theta, p1, p2,
+                            scalars, counts, status, 0, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_spectrum_quantities(const double* alphas, const double* betas, int64_t n, int r,
+                             double* rho, double* theta, double* p1, double* p2, double* scalars,
+                             int* status, void* stream) {
+  if (n < 1 || r < 0 || r > n) return RGSV_ERR_DIMENSION;
+  return launch_comparative(alphas, nullptr, betas, n, 0.0, nullptr, nullptr, rho, theta, p1, p2,
+                            scalars, nullptr, status, 1, r,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_entropy(const double* p, int64_t n, double* scalars, void* stream) {
+  if (n < 2) return RGSV_ERR_VALIDATION;
+  return launch_comparative(p, nullptr, nullptr, n, 0.0, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, nullptr, scalars, nullptr, nullptr, 2, 0,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t rgsv_svd_values_workspace_bytes(int rows, int cols) {
+  return (size_t)rows * cols * sizeof(double) + 256;
+}
+
+int rgsv_svd_values(const double* a, int64_t lda, int rows, int cols, double* sv, int* nsv,
+                    int* status, void* workspace, size_t workspace_bytes, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (rows < 1 || cols < 1) return RGSV_ERR_DIMENSION;
+  if (workspace_bytes < rgsv_svd_values_workspace_bytes(rows, cols)) return RGSV_ERR_WORKSPACE;
+  double* v = static_cast<double*>(workspace);
+  int nv, len;
+  if (rows <= cols) {
+    nv = rows;
+    len = cols;
+    if (int e = launch_copy_block(v, len, a, lda, rows, cols, 0, st)) return e;
+  } else {
+    nv = cols;
+    len = rows;
+    if (int e = launch_copy_block(v, len, a, lda, cols, rows, 1, st)) return e;
+  }
+  return launch_jacobi(v, len, nv, len, sv, nsv, v, len, 0, len, sv, nsv + 1, status, st);
+}
+
+int rgsv_gemm_gx(const double* a, int64_t lda, const double* bt, int64_t ldb, double* c,
+                 int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
+                 size_t scratch_bytes, void* stream) {
+  GemmArgs g;
+  g.A = a;
+  g.lda = lda;
+  g.B = bt;
+  g.ldb = ldb;
+  g.C = c;
+  g.ldc = ldc;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.scratch = static_cast<double*>(scratch);
+  g.scratch_bytes = scratch_bytes;
+  g.max_split = 32;
+  return gemm_gx(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_gemm_gtq(const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                  int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
+                  size_t scratch_bytes, void* stream) {
+  GemmArgs g;
+  g.A = a;
+  g.lda = lda;
+  g.B = b;
+  g.ldb = ldb;
+  g.C = c;
+  g.ldc = ldc;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.scratch = static_cast<double*>(scratch);
+  g.scratch_bytes = scratch_bytes;
+  g.max_split = kSMs;
+  return gemm_gtq(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv,
+                  double* rinv, double* rdiag, int* status, void* stream) {
+  return chol_inv(gram, k, kp, shift_rows, linv, rinv, nullptr, rdiag, nullptr, status,
+                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
+               void* workspace, size_t workspace_bytes, void* stream) {
+  if (rows < 1 || cols < 1) return RGSV_ERR_DIMENSION;
+  int parts = (int)(workspace_bytes / sizeof(double));
+  if (parts > 1024) parts = 1024;
+  if (parts < 1) return RGSV_ERR_WORKSPACE;
+  return launch_sumsq(a, lda, rows, cols, out, static_cast<double*>(workspace), parts,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

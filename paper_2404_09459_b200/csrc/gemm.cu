@@ -1,0 +1,463 @@
+// Skinny FP64 GEMMs of the rGSVD hot path (SURVEY.md §2b K1-K3, K5 Gram/TRSM):
+//
+//   gx : Y  (M x N)  = G (M x K) * X      with X given K-major as Xt (N x K)
+//        (sketch Y = G*Omega, power step Y = G*Qhat, CholQR TRSM Q = Y*Rinv,
+//         wide Gram B*B^T)
+//   gtq: C  (Mk x N) = Q^T (Mk x K) * G (K x N), reduction over the rows of
+//        both row-major operands (power step / projection B = Q^T G, CholQR
+//        Gram Y^T Y, wide TRSM Linv*B)
+//
+// Layout: every operand is row-major in HBM. A CTA = 1 producer warp (one
+// elected lane issues TMA for both operands of a 16-deep K chunk into a
+// STAGES-deep ring, 128B swizzle) + WM*WN DMMA warps. Fragment loads are
+// conflict-free: for gx both operands are K-major (8 rows x 4 consecutive
+// doubles per fragment); for gtq both are MN-major and the 4 K indices of a
+// k4 step are taken as rows {j, j+4, j+8, j+12} of the chunk so that the two
+// row pairs land in opposite halves of the swizzled bank space.
+//
+// Work decomposition: blockIdx.x enumerates `full` whole-K tiles first, then
+// the tail tiles split `split` ways along K; split units write partials that
+// k_reduce_splits sums in a fixed order (results are bitwise deterministic).
+#include "common.cuh"
+#include "rgsv_internal.h"
+
+namespace rgsv {
+
+struct Decomp {
+  int tiles_n;      // tiles along the output's N dimension
+  int full;         // units [0, full): tile = u, whole K range
+  int tail_tile0;   // first split tile
+  int split;        // splits per tail tile
+  int nchunks;      // 16-deep K chunks
+  int cps;          // chunks per split
+};
+
+RGSV_DI void decode_unit(const Decomp& d, int u, int& tile, int& c0, int& c1, int& s) {
+  if (u < d.full) {
+    tile = u;
+    c0 = 0;
+    c1 = d.nchunks;
+    s = -1;
+  } else {
+    int v = u - d.full;
+    tile = d.tail_tile0 + v / d.split;
+    s = v % d.split;
+    c0 = s * d.cps;
+    c1 = min(d.nchunks, c0 + d.cps);
+    if (c1 < c0) c1 = c0;
+  }
+}
+
+// ------------------------------------------------------------------- gx
+template <int MT, int NT, int WM, int WN, int STAGES, bool SUMSQ>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    k_gx(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX,
+         double* __restrict__ out, int64_t ld_out, double* __restrict__ part,
+         int64_t part_stride, int part_row0, int M, int N, Decomp d,
+         double* __restrict__ ss_out) {
+  constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN, NCW = WM * WN;
+  constexpr uint32_t G_BYTES = BM * 128, X_BYTES = BN * 128, STAGE = G_BYTES + X_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  __shared__ double red[NCW];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tile, c0, c1, split;
+  decode_unit(d, blockIdx.x, tile, c0, c1, split);
+  const int tm = tile / d.tiles_n, tn = tile % d.tiles_n;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int nk = c1 - c0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {  // producer
+    if (lane == 0) {
+      tma_prefetch(&tmG);
+      tma_prefetch(&tmX);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE);
+        uint8_t* st = smem + s * STAGE;
+        const int kx = (c0 + i) * 16;
+        tma_load_2d(st, &tmG, &full[s], kx, m0);
+        tma_load_2d(st + G_BYTES, &tmX, &full[s], kx, n0);
+      }
+    }
+    return;
+  }
+
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double ss = 0.0;
+  const bool do_ss = SUMSQ && wn == 0 && tn == 0;
+
+  for (int i = 0; i < nk; ++i) {
+    const int s = i % STAGES;
+    mbar_wait(&full[s], (i / STAGES) & 1);
+    const uint8_t* sg = smem + s * STAGE;
+    const uint8_t* sx = sg + G_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int kap = kk * 4 + t;
+      double a[MT], b[NT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        a[mt] = *reinterpret_cast<const double*>(sg + swz128_f64((wm * MT + mt) * 8 + g, kap));
+        if (SUMSQ && do_ss) ss = fma(a[mt], a[mt], ss);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        b[nt] = *reinterpret_cast<const double*>(sx + swz128_f64((wn * NT + nt) * 8 + g, kap));
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt], a[mt], b[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  double* o;
+  int64_t ldo;
+  int rbase;
+  if (split < 0) {
+    o = out;
+    ldo = ld_out;
+    rbase = 0;
+  } else {
+    o = part + split * part_stride;
+    ldo = ld_out;
+    rbase = part_row0;
+  }
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int row = m0 + (wm * MT + mt) * 8 + g;
+    if (row >= M) continue;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int col = n0 + (wn * NT + nt) * 8 + 2 * t;
+      double* p = o + (int64_t)(row - rbase) * ldo + col;
+      if (col + 1 < N) {
+        *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      } else if (col < N) {
+        p[0] = acc[mt][nt][0];
+      }
+    }
+  }
+  if (SUMSQ) {
+    ss = warp_sum(ss);
+    if (lane == 0) red[warp] = ss;
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32));
+    if (threadIdx.x == 0 && tn == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < NCW; ++w) tot += red[w];
+      ss_out[blockIdx.x] = tot;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ gtq
+template <int MT, int NT, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    k_gtq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmG,
+          double* __restrict__ out, int64_t ld_out, double* __restrict__ part,
+          int64_t part_stride, int Mk, int N, Decomp d) {
+  constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN, NCW = WM * WN;
+  constexpr int QBOX = BM / 16, GBOX = BN / 16;
+  constexpr uint32_t Q_BYTES = BM * 128, G_BYTES = BN * 128, STAGE = Q_BYTES + G_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tile, c0, c1, split;
+  decode_unit(d, blockIdx.x, tile, c0, c1, split);
+  const int tk = tile / d.tiles_n, tn = tile % d.tiles_n;
+  const int k0 = tk * BM, n0 = tn * BN;
+  const int nk = c1 - c0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmG);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], STAGE);
+        uint8_t* st = smem + s * STAGE;
+        const int y = (c0 + i) * 16;
+#pragma unroll 1
+        for (int b = 0; b < QBOX; ++b) tma_load_2d(st + b * 2048, &tmQ, &full[s], k0 + b * 16, y);
+#pragma unroll 1
+        for (int b = 0; b < GBOX; ++b)
+          tma_load_2d(st + Q_BYTES + b * 2048, &tmG, &full[s], n0 + b * 16, y);
+      }
+    }
+    return;
+  }
+
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int i = 0; i < nk; ++i) {
+    const int s = i % STAGES;
+    mbar_wait(&full[s], (i / STAGES) & 1);
+    const uint8_t* sq = smem + s * STAGE;
+    const uint8_t* sg = sq + Q_BYTES;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int rho = j + 4 * t;
+      double a[MT], b[NT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int c = (wm * MT + mt) * 8 + g;
+        a[mt] = *reinterpret_cast<const double*>(sq + (c >> 4) * 2048 + swz128_f64(rho, c & 15));
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = (wn * NT + nt) * 8 + g;
+        b[nt] = *reinterpret_cast<const double*>(sg + (c >> 4) * 2048 + swz128_f64(rho, c & 15));
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt], a[mt], b[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  double* o = split < 0 ? out : part + split * part_stride;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int row = k0 + (wm * MT + mt) * 8 + g;
+    if (row >= Mk) continue;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int col = n0 + (wn * NT + nt) * 8 + 2 * t;
+      double* p = o + (int64_t)row * ld_out + col;
+      if (col + 1 < N) {
+        *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      } else if (col < N) {
+        p[0] = acc[mt][nt][0];
+      }
+    }
+  }
+}
+
+// out[r][c] = sum_{s < S} part[s][r][c] for r < rows, c < cols (fixed order).
+__global__ void k_reduce_splits(double* __restrict__ out, int64_t ld, const double* __restrict__ part,
+                                int64_t part_stride, int S, int rows, int cols) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e / cols), c = static_cast<int>(e % cols);
+    const double* p = part + (int64_t)r * ld + c;
+    double acc = 0.0;
+    for (int s = 0; s < S; ++s) acc += p[s * part_stride];
+    out[(int64_t)r * ld + c] = acc;
+  }
+}
+
+// -------------------------------------------------------------- host side
+namespace {
+
+template <typename K>
+int set_smem(K kernel, size_t bytes) {
+  static thread_local const void* done[64];
+  static thread_local int ndone = 0;
+  for (int i = 0; i < ndone; ++i)
+    if (done[i] == reinterpret_cast<const void*>(kernel)) return 0;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
+    return RGSV_ERR_CUDA;
+  if (ndone < 64) done[ndone++] = reinterpret_cast<const void*>(kernel);
+  return 0;
+}
+
+// Plan the unit list for `tiles` output tiles over `nchunks` K chunks.
+Decomp plan_units(int tiles_m, int tiles_n, int nchunks, int max_split, int* units, int* S) {
+  Decomp d{};
+  const int tiles = tiles_m * tiles_n;
+  d.tiles_n = tiles_n;
+  d.nchunks = nchunks;
+  const int slots = kSMs;
+  // whole-K tiles fill complete waves; the remainder (rounded out to whole
+  // tile rows so split rows never overlap whole-K rows) is split along K.
+  const int waves = tiles / slots;
+  const int full = (waves * slots / tiles_n) * tiles_n;
+  const int tail = tiles - full;
+  int split = 1;
+  if (tail != 0) split = slots / tail;
+  if (split > max_split) split = max_split;
+  if (split > nchunks / 2) split = nchunks / 2;
+  if (split < 1) split = 1;
+  if (split == 1 || (waves > 0 && tail > slots * 3 / 4)) {
+    d.full = tiles;
+    d.tail_tile0 = tiles;
+    d.split = 1;
+    d.cps = nchunks;
+    *units = tiles;
+    *S = 0;
+  } else {
+    d.full = full;
+    d.tail_tile0 = full;
+    d.split = split;
+    d.cps = (nchunks + split - 1) / split;
+    *units = full + tail * split;
+    *S = split;
+  }
+  return d;
+}
+
+template <int MT, int NT, int WM, int WN, int STAGES, bool SUMSQ>
+int run_gx(const GemmArgs& a, cudaStream_t st) {
+  constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN;
+  CUtensorMap tmG, tmX;
+  if (make_tmap_2d(&tmG, a.A, a.K, a.M, a.lda, 16, BM, 8)) return RGSV_ERR_CUDA;
+  if (make_tmap_2d(&tmX, a.B, a.K, a.N, a.ldb, 16, BN, 8)) return RGSV_ERR_CUDA;
+  const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const int nchunks = (int)((a.K + 15) / 16);
+  int units, S;
+  Decomp d = plan_units(tiles_m, tiles_n, nchunks, a.max_split, &units, &S);
+  if (SUMSQ && tiles_n != 1) return RGSV_ERR_DIMENSION;
+  int part_row0 = 0;
+  if (S > 0) {
+    part_row0 = (d.tail_tile0 / tiles_n) * BM;
+    const size_t need = (size_t)S * (size_t)(a.M - part_row0) * a.ldc * sizeof(double);
+    if (need > a.scratch_bytes) return RGSV_ERR_WORKSPACE;
+  }
+  const int64_t part_stride = (int64_t)(a.M - part_row0) * a.ldc;
+  const size_t smem = STAGES * (BM + BN) * 128 + 2 * STAGES * 8 + 1024;
+  auto kern = k_gx<MT, NT, WM, WN, STAGES, SUMSQ>;
+  if (int e = set_smem(kern, smem)) return e;
+  kern<<<units, (WM * WN + 1) * 32, smem, st>>>(tmG, tmX, a.C, a.ldc, a.scratch, part_stride,
+                                                 part_row0, (int)a.M, (int)a.N, d, a.ss_out);
+  note_launch();
+  if (S > 0) {
+    const int rows = (int)(a.M - part_row0);
+    const int64_t total = (int64_t)rows * a.N;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+    k_reduce_splits<<<blocks, 256, 0, st>>>(a.C + (int64_t)part_row0 * a.ldc, a.ldc, a.scratch,
+                                            part_stride, S, rows, (int)a.N);
+    note_launch();
+  }
+  if (a.ss_units) *a.ss_units = units;
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+template <int MT, int NT, int WM, int WN, int STAGES>
+int run_gtq(const GemmArgs& a, cudaStream_t st) {
+  constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN;
+  CUtensorMap tmQ, tmG;
+  // Q: K rows x M cols (ld lda); G: K rows x N cols (ld ldb)
+  if (make_tmap_2d(&tmQ, a.A, a.M, a.K, a.lda, 16, 16, 8)) return RGSV_ERR_CUDA;
+  if (make_tmap_2d(&tmG, a.B, a.N, a.K, a.ldb, 16, 16, 8)) return RGSV_ERR_CUDA;
+  const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const int nchunks = (int)((a.K + 15) / 16);
+  const int tiles = tiles_m * tiles_n;
+  Decomp d{};
+  d.tiles_n = tiles_n;
+  d.nchunks = nchunks;
+  int split = kSMs / tiles;
+  if (split > a.max_split) split = a.max_split;
+  if (split > nchunks) split = nchunks;
+  if (split < 1) split = 1;
+  int units = tiles, S = 0;
+  if (split == 1) {
+    d.full = tiles;
+    d.tail_tile0 = tiles;
+    d.split = 1;
+    d.cps = nchunks;
+  } else {
+    d.full = 0;
+    d.tail_tile0 = 0;
+    d.split = split;
+    d.cps = (nchunks + split - 1) / split;
+    units = tiles * split;
+    S = split;
+    const size_t need = (size_t)S * a.M * a.ldc * sizeof(double);
+    if (need > a.scratch_bytes) return RGSV_ERR_WORKSPACE;
+  }
+  const int64_t part_stride = (int64_t)a.M * a.ldc;
+  const size_t smem = STAGES * (BM + BN) * 128 + 2 * STAGES * 8 + 1024;
+  auto kern = k_gtq<MT, NT, WM, WN, STAGES>;
+  if (int e = set_smem(kern, smem)) return e;
+  kern<<<units, (WM * WN + 1) * 32, smem, st>>>(tmQ, tmG, a.C, a.ldc, a.scratch, part_stride,
+                                                 (int)a.M, (int)a.N, d);
+  note_launch();
+  if (S > 0) {
+    const int64_t total = (int64_t)a.M * a.N;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+    k_reduce_splits<<<blocks, 256, 0, st>>>(a.C, a.ldc, a.scratch, part_stride, S, (int)a.M,
+                                            (int)a.N);
+    note_launch();
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+}  // namespace
+
+// C (M x N) = A (M x K) * B^T  with B given as N x K (both K-major).
+int gemm_gx(const GemmArgs& a, cudaStream_t st) {
+  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return RGSV_ERR_DIMENSION;
+  if (a.ss_out) {
+    if (a.N <= 16) return run_gx<2, 2, 8, 1, 6, true>(a, st);
+    if (a.N <= 32) return run_gx<2, 4, 8, 1, 6, true>(a, st);
+    if (a.N <= 64) return run_gx<4, 4, 4, 2, 6, true>(a, st);
+    if (a.N <= 128) return run_gx<4, 8, 4, 2, 5, true>(a, st);
+    return RGSV_ERR_DIMENSION;
+  }
+  if (a.N <= 16) return run_gx<2, 2, 8, 1, 6, false>(a, st);
+  if (a.N <= 32) return run_gx<2, 4, 8, 1, 6, false>(a, st);
+  if (a.N <= 64) return run_gx<4, 4, 4, 2, 6, false>(a, st);
+  return run_gx<4, 8, 4, 2, 5, false>(a, st);
+}
+
+// C (M x N) = A^T * B with A: K x M, B: K x N (both row-major, reduction over K rows).
+int gemm_gtq(const GemmArgs& a, cudaStream_t st) {
+  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return RGSV_ERR_DIMENSION;
+  if (a.N <= 16 && a.M <= 16) return run_gtq<1, 1, 2, 2, 6>(a, st);
+  if (a.N <= 32 && a.M <= 32) return run_gtq<2, 2, 2, 2, 6>(a, st);
+  if (a.N <= 64 && a.M <= 64) return run_gtq<4, 4, 2, 2, 6>(a, st);
+  if (a.M <= 16) return run_gtq<2, 4, 1, 8, 6>(a, st);
+  if (a.M <= 32) return run_gtq<2, 4, 2, 4, 6>(a, st);
+  if (a.M <= 64) return run_gtq<4, 4, 2, 4, 6>(a, st);
+  return run_gtq<4, 4, 4, 2, 6>(a, st);
+}
+
+}  // namespace rgsv

@@ -1,0 +1,63 @@
+// Internal (C++) interfaces shared by the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/rgsv_b200.h"
+
+namespace rgsv {
+
+// Generic skinny-GEMM launch description (see gemm.cu for the two shapes).
+struct GemmArgs {
+  const double* A = nullptr;
+  int64_t lda = 0;
+  const double* B = nullptr;
+  int64_t ldb = 0;
+  double* C = nullptr;
+  int64_t ldc = 0;
+  int64_t M = 0, N = 0, K = 0;
+  double* scratch = nullptr;  // split-K partials
+  size_t scratch_bytes = 0;
+  int max_split = 32;
+  double* ss_out = nullptr;  // gx only: per-unit sum of squares of A
+  int* ss_units = nullptr;
+};
+
+int gemm_gx(const GemmArgs& a, cudaStream_t st);
+int gemm_gtq(const GemmArgs& a, cudaStream_t st);
+
+// Cholesky of a k x k Gram (row-major, ld kp) with optional shift
+// 11 (rows k + k (k+1)) u trace (shifted CholeskyQR, Fukaya et al. 2020);
+// writes Linv = L^{-1} (kp x kp, identity padding), optionally its
+// transpose Rinv, R = L^T, and the diagonal of R. status[0] |= 1 on breakdown.
+int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
+             double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st);
+
+struct Workspace {
+  char* base;
+  size_t bytes;
+  size_t used;
+  void* take(size_t n) {
+    size_t off = (used + 255) & ~size_t(255);
+    if (off + n > bytes) return nullptr;
+    used = off + n;
+    return base + off;
+  }
+};
+
+// Shifted CholeskyQR3 of a tall row-major m x kp block (k real columns,
+// zero padding). Input y is overwritten; the orthonormal factor is returned
+// in *q_out (one of y / tmp). rdiag (k) receives diag(R).
+int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram, double* linv,
+                 double* rdiag, double* scratch, size_t scratch_bytes, int* status,
+                 double** q_out, cudaStream_t st);
+
+// Shifted CholeskyQR3 of Z = B^T where B is kp x n row-major (ld ldn):
+// returns Qhat^T (kp x n) in *qt_out (one of b / tmp).
+int cholqr3_wide(double* b, double* tmp, int64_t n, int64_t ldn, int k, int kp, double* gram,
+                 double* linv, double* rinv, double* rdiag, double* scratch, size_t scratch_bytes,
+                 int* status, double** qt_out, cudaStream_t st);
+
+}  // namespace rgsv

@@ -1,0 +1,387 @@
+// Small-GSVD and comparative-analysis kernels.
+//
+//  k_stack        S = [B1[:l1]; B2[:l2]]          (engine.py:257 vstack)
+//  k_copy_block   strided block copy / transpose  (L-block extraction)
+//  k_jacobi_rows  one-sided (Hestenes) Jacobi on the rows of an L block:
+//                 singular values with high relative accuracy, the role of
+//                 LAPACK gesdd in engine._singular_values (engine.py:228-231)
+//  k_comparative  spectrum completion (merged branch, engine.py:208-223),
+//                 classification + snapping (engine.py:164-186), rho, theta,
+//                 P1/P2 and D1/D2 (analysis.py:37-79) in one CTA
+//  k_sumsq_*      deterministic two-stage sum of squares (core.sum_sq)
+#include <math.h>
+
+#include "common.cuh"
+#include "rgsv_internal.h"
+
+namespace rgsv {
+
+__global__ void k_stack(double* __restrict__ s, int64_t lds, const double* __restrict__ b1,
+                        int64_t ld1, int l1, const double* __restrict__ b2, int64_t ld2, int l2,
+                        int lp, int64_t n) {
+  const int64_t total = (int64_t)lp * lds;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / lds);
+    const int64_t c = e % lds;
+    double v = 0.0;
+    if (c < n) {
+      if (r < l1) v = b1[(int64_t)r * ld1 + c];
+      else if (r < l1 + l2) v = b2[(int64_t)(r - l1) * ld2 + c];
+    }
+    s[e] = v;
+  }
+}
+
+// dst (rows x cols, ldd) = src block (optionally transposed: dst[i][j] = src[j][i]).
+__global__ void k_copy_block(double* __restrict__ dst, int64_t ldd, const double* __restrict__ src,
+                             int64_t lds, int rows, int cols, int transpose) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    dst[(int64_t)i * ldd + j] = transpose ? src[(int64_t)j * lds + i] : src[(int64_t)i * lds + j];
+  }
+}
+
+struct JacobiJob {
+  double* v;      // nv x len vectors (rows), modified in place
+  int64_t ld;
+  int nv;
+  int len;
+  double* sv_out;  // min(nv, len) values, descending
+  int* nsv_out;
+};
+
+RGSV_DI int rr_index(int p, int round, int nplayers) {
+  return p == 0 ? 0 : 1 + ((p - 1 + round) % (nplayers - 1));
+}
+
+constexpr int kJacobiMaxVec = 2048;
+
+__global__ void __launch_bounds__(1024) k_jacobi_rows(JacobiJob j0, JacobiJob j1, int max_sweeps,
+                                                       int* __restrict__ status) {
+  const JacobiJob J = blockIdx.x == 0 ? j0 : j1;
+  __shared__ double nrm[kJacobiMaxVec];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int nout = J.nv < J.len ? J.nv : J.len;
+  if (J.nv <= 0 || J.len <= 0) {
+    if (tid == 0) *J.nsv_out = 0;
+    return;
+  }
+  const int nve = J.nv + (J.nv & 1);
+  const double tol = fmax(1e-15, sqrt((double)J.len) * 2.220446049250313e-16);
+  bool converged = (J.nv == 1);
+  for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < nve - 1; ++round) {
+      for (int p = warp; p < nve / 2; p += nwarps) {
+        const int a = rr_index(p, round, nve), b = rr_index(nve - 1 - p, round, nve);
+        if (a >= J.nv || b >= J.nv) continue;
+        double* va = J.v + (int64_t)a * J.ld;
+        double* vb = J.v + (int64_t)b * J.ld;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int e = lane; e < J.len; e += 32) {
+          const double x = va[e], y = vb[e];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int e = lane; e < J.len; e += 32) {
+            const double x = va[e], y = vb[e];
+            va[e] = c * x - s * y;
+            vb[e] = s * x + c * y;
+          }
+          rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    converged = !__syncthreads_or(rotated);
+  }
+  if (!converged) {
+    if (tid == 0) atomicOr(status, RGSV_ST_JACOBI);
+  }
+  for (int i = warp; i < J.nv; i += nwarps) {
+    const double* vi = J.v + (int64_t)i * J.ld;
+    double s = 0.0;
+    for (int e = lane; e < J.len; e += 32) s = fma(vi[e], vi[e], s);
+    s = warp_sum(s);
+    if (lane == 0) nrm[i] = sqrt(s);
+  }
+  __syncthreads();
+  for (int i = tid; i < J.nv; i += blockDim.x) {
+    const double x = nrm[i];
+    int rank = 0;
+    for (int j = 0; j < J.nv; ++j) {
+      const double y = nrm[j];
+      rank += (y > x) || (y == x && j < i);
+    }
+    if (rank < nout) J.sv_out[rank] = x;
+  }
+  if (tid == 0) *J.nsv_out = nout;
+}
+
+// ---------------------------------------------------------- comparative
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w = 0; w < nw; ++w) tot += red[w];  // fixed order, every thread
+  return tot;
+}
+
+// mode 0: from L-block singular values (complete + classify + snap);
+// mode 1: from a given spectrum (sv1 = alphas, sv2 = betas, r = r_given);
+// mode 2: entropy of a given probability vector sv1 (scalars[0] = D,
+//         scalars[2] = sum p).
+__global__ void __launch_bounds__(1024) k_comparative(
+    const double* __restrict__ sv1, const int* __restrict__ nsv, const double* __restrict__ sv2,
+    int64_t n, double tol, double* __restrict__ A, double* __restrict__ B,
+    double* __restrict__ rho, double* __restrict__ theta, double* __restrict__ p1,
+    double* __restrict__ p2, double* __restrict__ scalars, int* __restrict__ counts,
+    int* __restrict__ status, int mode, int r_given) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (mode == 2) {
+    double sp = 0.0, ent = 0.0;
+    for (int64_t i = tid; i < n; i += nt) {
+      const double q = sv1[i];
+      sp += q;
+      if (q > 0.0) ent = fma(q, log(q), ent);
+    }
+    sp = block_sum(sp, red);
+    ent = block_sum(ent, red);
+    if (tid == 0) {
+      double d = -ent / log((double)n);
+      scalars[0] = fmin(fmax(d, 0.0), 1.0) + 0.0;
+      scalars[2] = sp;
+    }
+    return;
+  }
+  if (mode == 1) {
+    double sa = 0.0, sb = 0.0;
+    const double quarter_pi = 0.7853981633974483;
+    for (int64_t i = tid; i < n; i += nt) {
+      const double a = sv1[i], b = sv2[i];
+      rho[i] = (i < r_given) ? __longlong_as_double(0x7ff0000000000000LL) : a / b;
+      theta[i] = atan2(a, b) - quarter_pi;
+      sa = fma(a, a, sa);
+      sb = fma(b, b, sb);
+    }
+    sa = block_sum(sa, red);
+    sb = block_sum(sb, red);
+    if (!(sa > 0.0) || !(sb > 0.0)) {
+      if (tid == 0) atomicOr(status, RGSV_ST_DEGENERATE);
+      return;
+    }
+    double e1 = 0.0, e2 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int64_t i = tid; i < n; i += nt) {
+      const double a = sv1[i], b = sv2[i];
+      const double q1 = a * a / sa, q2 = b * b / sb;
+      p1[i] = q1;
+      p2[i] = q2;
+      s1 += q1;
+      s2 += q2;
+      if (q1 > 0.0) e1 = fma(q1, log(q1), e1);
+      if (q2 > 0.0) e2 = fma(q2, log(q2), e2);
+    }
+    s1 = block_sum(s1, red);
+    s2 = block_sum(s2, red);
+    e1 = block_sum(e1, red);
+    e2 = block_sum(e2, red);
+    if (tid == 0) {
+      const double ln = log((double)n);
+      scalars[0] = fmin(fmax(-e1 / ln, 0.0), 1.0) + 0.0;
+      scalars[1] = fmin(fmax(-e2 / ln, 0.0), 1.0) + 0.0;
+      scalars[2] = s1;
+      scalars[3] = s2;
+    }
+    return;
+  }
+  const int64_t c1 = nsv[0], c2 = nsv[1];
+  double cr = 0.0, cza = 0.0;
+  for (int64_t i = tid; i < n; i += nt) {
+    const double ar = (i < c1) ? fmin(fmax(sv1[i], 0.0), 1.0) : 0.0;
+    const double br = (i >= n - c2) ? fmin(fmax(sv2[n - 1 - i], 0.0), 1.0) : 0.0;
+    double a, b;
+    // numpy evaluates sqrt(1.0 - x**2) with two roundings; keep them
+    // (no FMA contraction) so the completed spectrum matches bit for bit
+    if (ar <= br) {
+      a = ar;
+      b = sqrt(__dsub_rn(1.0, __dmul_rn(ar, ar)));
+    } else {
+      a = sqrt(__dsub_rn(1.0, __dmul_rn(br, br)));
+      b = br;
+    }
+    A[i] = a;
+    B[i] = b;
+    cr += (b < tol) ? 1.0 : 0.0;
+    cza += (a < tol) ? 1.0 : 0.0;
+  }
+  const int64_t r = (int64_t)block_sum(cr, red);
+  const int64_t za = (int64_t)block_sum(cza, red);
+  const int64_t s = n - r - za;
+  if (s < 0) {
+    if (tid == 0) {
+      atomicOr(status, RGSV_ST_CLASSIFY);
+      counts[0] = (int)r;
+      counts[1] = (int)s;
+    }
+    return;
+  }
+  double sa = 0.0, sb = 0.0;
+  const double quarter_pi = 0.7853981633974483;  // math.pi / 4
+  for (int64_t i = tid; i < n; i += nt) {
+    double a = A[i], b = B[i];
+    if (i < r) {
+      b = 0.0;
+      a = 1.0;
+    }
+    if (za && i >= n - za) {
+      a = 0.0;
+      b = 1.0;
+    }
+    A[i] = a;
+    B[i] = b;
+    rho[i] = (i < r) ? __longlong_as_double(0x7ff0000000000000LL) : a / b;
+    theta[i] = atan2(a, b) - quarter_pi;
+    sa = fma(a, a, sa);
+    sb = fma(b, b, sb);
+  }
+  sa = block_sum(sa, red);
+  sb = block_sum(sb, red);
+  if (tid == 0) {
+    counts[0] = (int)r;
+    counts[1] = (int)s;
+  }
+  if (!(sa > 0.0) || !(sb > 0.0)) {
+    if (tid == 0) atomicOr(status, RGSV_ST_DEGENERATE);
+    return;
+  }
+  double s1 = 0.0, s2 = 0.0, e1 = 0.0, e2 = 0.0;
+  for (int64_t i = tid; i < n; i += nt) {
+    const double a = A[i], b = B[i];
+    const double q1 = a * a / sa, q2 = b * b / sb;
+    p1[i] = q1;
+    p2[i] = q2;
+    s1 += q1;
+    s2 += q2;
+    if (q1 > 0.0) e1 = fma(q1, log(q1), e1);
+    if (q2 > 0.0) e2 = fma(q2, log(q2), e2);
+  }
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  e1 = block_sum(e1, red);
+  e2 = block_sum(e2, red);
+  if (tid == 0) {
+    const double ln = log((double)n);
+    double d1 = -e1 / ln, d2 = -e2 / ln;
+    d1 = fmin(fmax(d1, 0.0), 1.0) + 0.0;
+    d2 = fmin(fmax(d2, 0.0), 1.0) + 0.0;
+    scalars[0] = d1;
+    scalars[1] = d2;
+    scalars[2] = s1;
+    scalars[3] = s2;
+    if (n < 2 || fabs(s1 - 1.0) > 1e-10 || fabs(s2 - 1.0) > 1e-10)
+      atomicOr(status, RGSV_ST_NOT_NORMALIZED);
+  }
+}
+
+// ------------------------------------------------------------- sum of squares
+__global__ void k_sumsq_partial(const double* __restrict__ a, int64_t lda, int64_t rows,
+                                int64_t cols, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[(e / cols) * lda + (e % cols)];
+    s = fma(x, x, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_sum_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ------------------------------------------------------------ host wrappers
+int launch_stack(double* s, int64_t lds, const double* b1, int64_t ld1, int l1, const double* b2,
+                 int64_t ld2, int l2, int lp, int64_t n, cudaStream_t st) {
+  const int64_t total = (int64_t)lp * lds;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+  if (blocks < 1) blocks = 1;
+  k_stack<<<blocks, 256, 0, st>>>(s, lds, b1, ld1, l1, b2, ld2, l2, lp, n);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+int launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
+                      int transpose, cudaStream_t st) {
+  const int64_t total = (int64_t)rows * cols;
+  if (total <= 0) return 0;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+  k_copy_block<<<blocks, 256, 0, st>>>(dst, ldd, src, lds, rows, cols, transpose);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+int launch_jacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, double* v2,
+                  int64_t ld2, int nv2, int len2, double* sv2, int* nsv2, int* status,
+                  cudaStream_t st) {
+  if (nv1 > kJacobiMaxVec || nv2 > kJacobiMaxVec) return RGSV_ERR_DIMENSION;
+  JacobiJob a{v1, ld1, nv1, len1, sv1, nsv1};
+  JacobiJob b{v2, ld2, nv2, len2, sv2, nsv2};
+  k_jacobi_rows<<<2, 1024, 0, st>>>(a, b, 60, status);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+int launch_comparative(const double* sv1, const int* nsv, const double* sv2, int64_t n, double tol,
+                       double* a, double* b, double* rho, double* theta, double* p1, double* p2,
+                       double* scalars, int* counts, int* status, int mode, int r_given,
+                       cudaStream_t st) {
+  k_comparative<<<1, 1024, 0, st>>>(sv1, nsv, sv2, n, tol, a, b, rho, theta, p1, p2, scalars,
+                                    counts, status, mode, r_given);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+int launch_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
+                 double* part, int max_parts, cudaStream_t st) {
+  int64_t total = rows * cols;
+  int blocks = (int)((total + 1023) / 1024);
+  if (blocks > max_parts) blocks = max_parts;
+  if (blocks < 1) blocks = 1;
+  k_sumsq_partial<<<blocks, 256, 0, st>>>(a, lda, rows, cols, part);
+  note_launch();
+  k_sum_final<<<1, 256, 0, st>>>(part, blocks, out);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+int launch_sum(const double* part, int n, double* out, cudaStream_t st) {
+  k_sum_final<<<1, 256, 0, st>>>(part, n, out);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+}  // namespace rgsv

@@ -1,0 +1,258 @@
+"""Device-side orchestration of the rGSVD hot path.
+
+Owns the device buffers of a pair (cached per shape in a ``PairPlan``),
+issues the C-ABI calls on CUDA streams, and brings every small result back
+in ONE device->host copy. Matrices live in HBM as row-major float64 with an
+even row pitch (TMA needs 16-byte pitches); bases are padded to
+kp = ceil16(k) columns with exact zeros.
+
+Stream layout for a pair: the G1 chain (sketch -> CholQR3 -> q power
+iterations -> projection) runs on the caller's stream and the G2 chain on
+a side stream concurrently, so the single-CTA Cholesky steps of one chain
+overlap the DMMA GEMMs of the other; the small GSVD and the fused
+comparative kernel run after the join.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._native import check, lib, require_device
+from .errors import DimensionError, ValidationError
+
+SEED_MASK = (1 << 64) - 1
+F64 = torch.float64
+
+
+def ceil16(x: int) -> int:
+    return (x + 15) // 16 * 16
+
+
+def vp(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def sp(stream: torch.cuda.Stream) -> ctypes.c_void_p:
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+@dataclass
+class DevMatrix:
+    """Row-major float64 matrix in HBM: ``t`` is a rows x cols view whose row
+    stride ``ld`` is even (TMA row pitch)."""
+
+    t: torch.Tensor
+    rows: int
+    cols: int
+
+    @property
+    def ld(self) -> int:
+        return self.t.stride(0)
+
+
+def _even(x: int) -> int:
+    return x + (x & 1)
+
+
+def to_device(a, name: str = "matrix") -> DevMatrix:
+    """Validate shape/field like core.as_matrix (core.py:43-57) and place
+    the matrix in HBM (no copy when it already is a suitable CUDA tensor).
+    Finiteness is checked on the device by the fused sum-of-squares pass."""
+    require_device()
+    if isinstance(a, DevMatrix):
+        return a
+    if isinstance(a, torch.Tensor):
+        t = a
+        if t.dim() != 2:
+            raise DimensionError(f"{name} must be 2-D, got shape {tuple(t.shape)}")
+        rows, cols = t.shape
+        if rows < 1 or cols < 1:
+            raise DimensionError(f"{name} must have positive dimensions, got {tuple(t.shape)}")
+        if t.is_complex():
+            raise ValidationError(f"{name}: complex matrices are not supported by the B200 path")
+        if t.dtype != F64:
+            t = t.to(F64)
+        if t.device.type != "cuda":
+            t = t.to("cuda")
+        if (t.stride(1) == 1 and t.stride(0) >= cols and t.stride(0) % 2 == 0
+                and t.data_ptr() % 16 == 0):
+            return DevMatrix(t, rows, cols)
+        dev = torch.zeros((rows, _even(cols)), dtype=F64, device="cuda")
+        dev[:, :cols].copy_(t)
+        return DevMatrix(dev[:, :cols], rows, cols)
+    arr = np.asarray(a)
+    if arr.ndim != 2:
+        raise DimensionError(f"{name} must be 2-D, got shape {arr.shape}")
+    if arr.shape[0] < 1 or arr.shape[1] < 1:
+        raise DimensionError(f"{name} must have positive dimensions, got {arr.shape}")
+    if np.iscomplexobj(arr):
+        raise ValidationError(f"{name}: complex matrices are not supported by the B200 path")
+    rows, cols = arr.shape
+    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
+    if cols % 2 == 0:
+        dev = torch.empty((rows, cols), dtype=F64, device="cuda")
+        dev.copy_(host, non_blocking=host.is_pinned())
+    else:
+        dev = torch.zeros((rows, cols + 1), dtype=F64, device="cuda")
+        dev[:, :cols].copy_(host)
+        dev = dev[:, :cols]
+    return DevMatrix(dev, rows, cols)
+
+
+def omega_host(n: int, k: int, seed: int) -> np.ndarray:
+    """The reference's Gaussian test matrix: one block of width k drawn from
+    default_rng(seed & (2^64 - 1)) (rangefinder.py:101,112)."""
+    return np.random.default_rng(int(seed) & SEED_MASK).standard_normal((n, k))
+
+
+# ----------------------------------------------------------------- results
+class _Packed:
+    """One device buffer + one pinned host mirror holding every small output
+    of a pair, so a single D2H copy returns all of them."""
+
+    def __init__(self, n: int, k1: int, k2: int):
+        self.n = n
+        f = [("stats1", 2), ("stats2", 2), ("scalars", 4), ("sv1", max(k1, 1)),
+             ("sv2", max(k2, 1)), ("alphas", n), ("betas", n), ("rho", n), ("theta", n),
+             ("p1", n), ("p2", n), ("rdiag1", max(k1, 1)), ("rdiag2", max(k2, 1))]
+        ints = [("status", 1), ("nsv", 2), ("counts", 2)]
+        self.off = {}
+        pos = 0
+        for name, cnt in f:
+            self.off[name] = ("f", pos, cnt)
+            pos += cnt * 8
+        for name, cnt in ints:
+            self.off[name] = ("i", pos, cnt)
+            pos += cnt * 4
+        self.nbytes = (pos + 15) // 16 * 16
+        self.dev = torch.zeros(self.nbytes, dtype=torch.uint8, device="cuda")
+        self.host = torch.zeros(self.nbytes, dtype=torch.uint8, pin_memory=True)
+        self.hnp = self.host.numpy()
+
+    def d(self, name) -> torch.Tensor:
+        kind, pos, cnt = self.off[name]
+        width = 8 if kind == "f" else 4
+        view = self.dev[pos:pos + cnt * width]
+        return view.view(F64 if kind == "f" else torch.int32)
+
+    def h(self, name) -> np.ndarray:
+        kind, pos, cnt = self.off[name]
+        dt = np.float64 if kind == "f" else np.int32
+        return self.hnp[pos:pos + cnt * (8 if kind == "f" else 4)].view(dt)
+
+
+@dataclass
+class MatrixOut:
+    q: torch.Tensor      # m x kp (device)
+    b: torch.Tensor      # kp x ldb (device)
+    k: int
+
+
+class SketchPlan:
+    """Buffers for one matrix chain (m x n, rank k)."""
+
+    def __init__(self, m: int, n: int, k: int):
+        self.m, self.n, self.k = m, n, k
+        self.kp = ceil16(k)
+        self.ldb = ceil16(n)
+        L = lib()
+        self.ws_bytes = int(L.rgsv_sketch_workspace_bytes(m, n, k))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
+        self.q = torch.zeros((m, self.kp), dtype=F64, device="cuda")
+        self.b = torch.zeros((self.kp, self.ldb), dtype=F64, device="cuda")
+        self.om_host = torch.zeros((self.kp, self.ldb), dtype=F64, pin_memory=True)
+        self.om_dev = torch.zeros((self.kp, self.ldb), dtype=F64, device="cuda")
+
+    def upload_omega(self, seed: int, stream) -> None:
+        om = omega_host(self.n, self.k, seed)
+        self.om_host[: self.k, : self.n].copy_(torch.from_numpy(om.T))
+        with torch.cuda.stream(stream):
+            self.om_dev.copy_(self.om_host, non_blocking=True)
+
+    def launch(self, g: DevMatrix, q_iters: int, stats: torch.Tensor, rdiag: torch.Tensor,
+               status: torch.Tensor, stream) -> None:
+        rc = lib().rgsv_sketch_project(
+            vp(g.t), g.ld, g.rows, g.cols, vp(self.om_dev), self.ldb, self.k, q_iters,
+            vp(self.q), vp(self.b), self.ldb, vp(stats), vp(rdiag), vp(status), vp(self.ws),
+            self.ws_bytes, sp(stream))
+        check(rc, "rgsv_sketch_project")
+
+
+class PairPlan:
+    """Cached buffers for a pair of shapes (m, p, n) at ranks (k1, k2)."""
+
+    def __init__(self, m: int, p: int, n: int, k1: int, k2: int):
+        self.m, self.p, self.n, self.k1, self.k2 = m, p, n, k1, k2
+        self.s1 = SketchPlan(m, n, k1)
+        self.s2 = SketchPlan(p, n, k2)
+        self.small_bytes = int(lib().rgsv_small_gsvd_workspace_bytes(k1, k2, n))
+        self.small_ws = torch.empty(self.small_bytes, dtype=torch.uint8, device="cuda")
+        self.pk = _Packed(n, k1, k2)
+        self.side = torch.cuda.Stream()
+
+    def run(self, g1: DevMatrix, g2: DevMatrix, seed: int, q_iters: int, classify_tol: float,
+            sync: bool = True):
+        L = lib()
+        main = torch.cuda.current_stream()
+        pk = self.pk
+        pk.d("status").zero_()
+        self.s1.upload_omega(seed, main)
+        self.s2.upload_omega(seed + 1, main)  # engine.py:252-253
+        self.side.wait_stream(main)
+        self.s1.launch(g1, q_iters, pk.d("stats1"), pk.d("rdiag1"), pk.d("status"), main)
+        self.s2.launch(g2, q_iters, pk.d("stats2"), pk.d("rdiag2"), pk.d("status"), self.side)
+        main.wait_stream(self.side)
+        rc = L.rgsv_small_gsvd(vp(self.s1.b), self.s1.ldb, self.k1, vp(self.s2.b), self.s2.ldb,
+                               self.k2, self.n, vp(pk.d("sv1")), vp(pk.d("sv2")),
+                               vp(pk.d("nsv")), vp(pk.d("status")), vp(self.small_ws),
+                               self.small_bytes, sp(main))
+        check(rc, "rgsv_small_gsvd")
+        rc = L.rgsv_comparative(vp(pk.d("sv1")), vp(pk.d("nsv")), vp(pk.d("sv2")), self.n,
+                                float(classify_tol), vp(pk.d("alphas")), vp(pk.d("betas")),
+                                vp(pk.d("rho")), vp(pk.d("theta")), vp(pk.d("p1")),
+                                vp(pk.d("p2")), vp(pk.d("scalars")), vp(pk.d("counts")),
+                                vp(pk.d("status")), sp(main))
+        check(rc, "rgsv_comparative")
+        pk.host.copy_(pk.dev, non_blocking=True)
+        if sync:
+            main.synchronize()
+        return pk
+
+
+_PLANS: dict = {}
+
+
+def pair_plan(m: int, p: int, n: int, k1: int, k2: int) -> PairPlan:
+    key = (torch.cuda.current_device(), m, p, n, k1, k2)
+    plan = _PLANS.get(key)
+    if plan is None:
+        if len(_PLANS) > 8:
+            _PLANS.clear()
+        plan = PairPlan(m, p, n, k1, k2)
+        _PLANS[key] = plan
+    return plan
+
+
+def residual_history(gf2: float, energy: float) -> list:
+    """[||G||_F, sqrt(max(||G||^2 - captured, 0))] (rangefinder.py:94,126-127)."""
+    return [math.sqrt(gf2), math.sqrt(max(gf2 - energy, 0.0))]
+
+
+def device_sumsq(g: DevMatrix) -> float:
+    """||G||_F^2 on the device (core.sum_sq, core.py:115-125)."""
+    out = torch.zeros(1, dtype=F64, device="cuda")
+    ws = torch.empty(1024, dtype=F64, device="cuda")
+    rc = lib().rgsv_sumsq(vp(g.t), g.ld, g.rows, g.cols, vp(out), vp(ws), ws.numel() * 8,
+                          sp(torch.cuda.current_stream()))
+    check(rc, "rgsv_sumsq")
+    return float(out.item())
+
+
+__all__ = ["DevMatrix", "to_device", "pair_plan", "PairPlan", "SketchPlan", "omega_host",
+           "residual_history", "device_sumsq", "ceil16", "_native"]

@@ -1,0 +1,298 @@
+"""Generalized singular values of a matrix pair (reference ``rgsv/engine.py``).
+
+``compute_gsv`` / ``compare`` run the whole randomized pipeline on the B200
+(device.PairPlan): both range-finder chains, the stacked QR + Jacobi SVD of
+the L blocks and the fused spectrum/comparative kernel, with one packed
+device->host copy at the end. The result types, their invariants and the
+error behaviour follow the reference line by line (citations inline).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import device as _dev
+from ._native import ST_CHOL, ST_CLASSIFY, ST_JACOBI
+from .errors import (
+    ConvergenceError,
+    DimensionError,
+    RankDeficiencyError,
+    RecoveryError,
+    ValidationError,
+)
+from .rangefinder import BasisResult, ExtractionConfig, check_max_cols, single_block_width
+
+RANDOMIZED = "randomized"
+DIRECT = "direct"
+
+
+@dataclass(frozen=True)
+class GmpPair:
+    """A pair {g1 (m x n), g2 (p x n)} held in HBM (engine.py:31-90).
+
+    Construction validates shapes, the field (real only on the B200 path),
+    finiteness (device pass) and m + p >= n. The reference additionally runs
+    a dense SVD of the stacked pair to check sigma_min > 1e-12 sigma_max
+    (engine.py:55-61); that O((m+p) n^2) check is requested with
+    ``check_rank=True`` (default False: the reference's own benchmark plan
+    builds the large pairs unvalidated)."""
+
+    g1: object
+    g2: object
+    check_rank: bool = False
+
+    def __post_init__(self):
+        a = _dev.to_device(self.g1, "g1")
+        b = _dev.to_device(self.g2, "g2")
+        if a.cols != b.cols:
+            raise DimensionError(f"g1 has {a.cols} columns but g2 has {b.cols}")
+        n = a.cols
+        if a.rows + b.rows < n:
+            raise RankDeficiencyError(f"stacked pair has {a.rows + b.rows} rows < {n} columns")
+        for name, g in (("g1", a), ("g2", b)):
+            if not math.isfinite(_dev.device_sumsq(g)):
+                raise ValidationError(f"{name} contains non-finite entries")
+        object.__setattr__(self, "g1", a)
+        object.__setattr__(self, "g2", b)
+        if self.check_rank:
+            from .validation import stacked_extreme_singular_values
+
+            smax, smin = stacked_extreme_singular_values(a, b)
+            if smin <= 1e-12 * smax:
+                raise RankDeficiencyError(
+                    f"stacked pair is numerically rank deficient "
+                    f"(sigma_min/sigma_max = {smin / smax if smax else 0.0:.3e})")
+            object.__setattr__(self, "_stack_smax", smax)
+            object.__setattr__(self, "_stack_smin", smin)
+
+    @classmethod
+    def resident(cls, g1, g2) -> "GmpPair":
+        """Wrap device matrices without the validation passes (the bench
+        path: G already resident in HBM, validated once at creation)."""
+        pair = object.__new__(cls)
+        object.__setattr__(pair, "g1", _dev.to_device(g1, "g1"))
+        object.__setattr__(pair, "g2", _dev.to_device(g2, "g2"))
+        object.__setattr__(pair, "check_rank", False)
+        return pair
+
+    @property
+    def m(self) -> int:
+        return self.g1.rows
+
+    @property
+    def p(self) -> int:
+        return self.g2.rows
+
+    @property
+    def n(self) -> int:
+        return self.g1.cols
+
+    def stacked(self) -> np.ndarray:
+        return np.vstack([self.g1.t.cpu().numpy(), self.g2.t.cpu().numpy()])
+
+    @property
+    def stack_norm2(self) -> float:
+        if not hasattr(self, "_stack_smax"):
+            raise AttributeError("construct with check_rank=True to compute stacked norms")
+        return self._stack_smax
+
+    @property
+    def stack_pinv_norm(self) -> float:
+        if not hasattr(self, "_stack_smin"):
+            raise AttributeError("construct with check_rank=True to compute stacked norms")
+        return 1.0 / self._stack_smin
+
+
+@dataclass(frozen=True)
+class GsvSpectrum:
+    """Paired GSV sequences with block counts (engine.py:93-129); the
+    invariants are checked exactly as the reference does."""
+
+    alphas: np.ndarray
+    betas: np.ndarray
+    r: int
+    s: int
+
+    def __post_init__(self):
+        a = np.asarray(self.alphas, dtype=np.float64)
+        b = np.asarray(self.betas, dtype=np.float64)
+        if a.ndim != 1 or b.ndim != 1 or a.size != b.size or a.size == 0:
+            raise DimensionError("alphas and betas must be 1-D of equal, nonzero length")
+        n = a.size
+        if self.r < 0 or self.s < 0 or self.r + self.s > n:
+            raise ValidationError(f"invalid counts r={self.r}, s={self.s} for n={n}")
+        if np.any(a < 0) or np.any(a > 1) or np.any(b < 0) or np.any(b > 1):
+            raise ValidationError("GSVs must lie in [0, 1]")
+        if np.any(np.diff(a) > 1e-12) or np.any(np.diff(b) < -1e-12):
+            raise ValidationError("alphas must be nonincreasing and betas nondecreasing")
+        if float(np.max(np.abs(a**2 + b**2 - 1.0))) > 1e-12:
+            raise ValidationError("alpha_i^2 + beta_i^2 = 1 violated beyond 1e-12")
+        if np.any(b[: self.r] != 0.0) or np.any(a[self.r + self.s:] != 0.0):
+            raise ValidationError("classified-zero entries must be exactly 0")
+        object.__setattr__(self, "alphas", a)
+        object.__setattr__(self, "betas", b)
+
+    @property
+    def n(self) -> int:
+        return self.alphas.size
+
+
+@dataclass(frozen=True)
+class GsvOptions:
+    """Method selection and thresholds (engine.py:132-150)."""
+
+    extraction: ExtractionConfig = ExtractionConfig()
+    classify_tol: float = 1e-10
+    method: str = RANDOMIZED
+
+    def __post_init__(self):
+        if not 0 < self.classify_tol < 1e-2:
+            raise ValidationError(f"classify_tol must be in (0, 1e-2), got {self.classify_tol}")
+        if self.method not in (RANDOMIZED, DIRECT):
+            raise ValidationError(
+                f"method must be 'randomized' or 'direct', got {self.method!r}")
+
+
+@dataclass(frozen=True)
+class GsvdFactors:
+    """G1 = U diag(alpha) R, G2 = V diag(beta) R (engine.py:153-161)."""
+
+    u: np.ndarray
+    v: np.ndarray
+    r_factor: np.ndarray
+    spectrum: GsvSpectrum
+
+
+def classify_spectrum(alphas, betas, classify_tol: float = 1e-10) -> tuple[int, int]:
+    """(r, s) block counts with in-place snapping (engine.py:164-186).
+    Operates on caller-owned arrays, as the reference does; the device
+    pipeline performs the same classification inside its fused kernel."""
+    if not 0 < classify_tol < 1e-2:
+        raise ValidationError(f"classify_tol must be in (0, 1e-2), got {classify_tol}")
+    a = np.asarray(alphas)
+    b = np.asarray(betas)
+    n = a.size
+    r = int(np.count_nonzero(b < classify_tol))
+    za = int(np.count_nonzero(a < classify_tol))
+    s = n - r - za
+    if s < 0:
+        raise ValidationError("overlapping zero classifications; sequences not ordered?")
+    b[:r] = 0.0
+    a[:r] = 1.0
+    if za:
+        a[n - za:] = 0.0
+        b[n - za:] = 1.0
+    return r, s
+
+
+@dataclass
+class DeviceRun:
+    """Everything one device pipeline run produced (host copies of the
+    small outputs; bases and projections stay in HBM)."""
+
+    spectrum: GsvSpectrum | None
+    alphas: np.ndarray
+    betas: np.ndarray
+    r: int
+    s: int
+    rho: np.ndarray
+    theta: np.ndarray
+    p1: np.ndarray
+    p2: np.ndarray
+    d1: float
+    d2: float
+    psum: tuple
+    status: int
+    basis1: BasisResult
+    basis2: BasisResult
+    sv1: np.ndarray
+    sv2: np.ndarray
+    plan: object
+
+
+def _fixed_width(opts: GsvOptions, m: int, p: int, n: int) -> tuple[int, int]:
+    cfg = opts.extraction
+    check_max_cols(cfg, m, n)
+    check_max_cols(cfg, p, n)
+    w1 = single_block_width(cfg, m, n)
+    w2 = single_block_width(cfg, p, n)
+    if w1 is None or w2 is None:
+        raise ValidationError(
+            "the B200 pipeline runs the fixed-rank range finder: use "
+            "ExtractionConfig.fixed_rank(k, seed, power_iters) (max_cols <= blocksize, "
+            "trim_tol = 0); adaptive multi-block extraction is not implemented on the device yet")
+    if opts.method == DIRECT:
+        raise ValidationError("method='direct' is not implemented on the B200 path yet")
+    return w1, w2
+
+
+def run_device_pipeline(pair: GmpPair, opts: GsvOptions, *, sync: bool = True) -> DeviceRun:
+    """The randomized path of _run_pipeline + spectrum_from_l_blocks +
+    analysis, on the device (engine.py:245-275, analysis.py:82-102)."""
+    k1, k2 = _fixed_width(opts, pair.m, pair.p, pair.n)
+    plan = _dev.pair_plan(pair.m, pair.p, pair.n, k1, k2)
+    cfg = opts.extraction
+    pk = plan.run(pair.g1, pair.g2, cfg.seed, cfg.power_iters, opts.classify_tol, sync=sync)
+    return unpack(pk, plan, opts)
+
+
+def unpack(pk, plan, opts: GsvOptions) -> DeviceRun:
+    status = int(pk.h("status")[0])
+    st1, st2 = pk.h("stats1"), pk.h("stats2")
+    bases = []
+    for (gf2, energy), k, rd in ((st1, plan.k1, "rdiag1"), (st2, plan.k2, "rdiag2")):
+        if not math.isfinite(gf2):
+            raise ValidationError("g contains non-finite entries")
+        hist = _dev.residual_history(float(gf2), float(energy))
+        tol = opts.extraction.tol if opts.extraction.tol is not None else 1e-10 * hist[0]
+        bases.append(BasisResult(None, hist, hist[-1] < tol, 1, [k]))
+    if status & ST_CHOL:
+        raise RankDeficiencyError("CholeskyQR breakdown: a sketch or the stacked pair is "
+                                  "numerically rank deficient")
+    if status & ST_JACOBI:
+        raise ConvergenceError("Jacobi SVD of an L block did not converge")
+    r, s = (int(x) for x in pk.h("counts"))
+    if status & ST_CLASSIFY:
+        raise ValidationError("overlapping zero classifications; sequences not ordered?")
+    alphas = pk.h("alphas").copy()
+    betas = pk.h("betas").copy()
+    spec = GsvSpectrum(alphas, betas, r, s)
+    sc = pk.h("scalars")
+    nsv = pk.h("nsv")
+    return DeviceRun(spec, spec.alphas, spec.betas, r, s, pk.h("rho").copy(),
+                     pk.h("theta").copy(), pk.h("p1").copy(), pk.h("p2").copy(), float(sc[0]),
+                     float(sc[1]), (float(sc[2]), float(sc[3])), status, bases[0], bases[1],
+                     pk.h("sv1")[: nsv[0]].copy(), pk.h("sv2")[: nsv[1]].copy(), plan)
+
+
+def compute_gsv(pair: GmpPair, opts: GsvOptions | None = None) -> GsvSpectrum:
+    """GSV spectrum of a pair on the B200 (engine.py:264-275)."""
+    opts = opts or GsvOptions()
+    return run_device_pipeline(pair, opts).spectrum
+
+
+def recover_gsvd(pair: GmpPair, opts: GsvOptions | None = None) -> GsvdFactors:
+    """Full decomposition recovery (engine.py:294-362). Requires m, p >= n
+    (:304-307) and an R-tilde with n rows (:309-313); in the fixed-rank mode
+    with l1 + l2 < n (every BASELINE config) the reference
+    raises RecoveryError, and so does this path."""
+    opts = opts or GsvOptions()
+    m, p, n = pair.m, pair.p, pair.n
+    if m < n or p < n:
+        raise RecoveryError(f"full recovery needs m >= n and p >= n, got ({m}, {p}, {n})")
+    k1, k2 = _fixed_width(opts, m, p, n)
+    if min(k1 + k2, n) != n:
+        raise RecoveryError(
+            "compressed pair has fewer than n independent columns; "
+            "tighten the extraction tolerance")
+    raise RecoveryError("GSVD factor recovery with l1 + l2 >= n is not implemented on the "
+                        "B200 path yet")
+
+
+__all__ = ["GmpPair", "GsvSpectrum", "GsvOptions", "GsvdFactors", "classify_spectrum",
+           "compute_gsv", "recover_gsvd", "run_device_pipeline", "RANDOMIZED", "DIRECT",
+           "dataclasses"]
