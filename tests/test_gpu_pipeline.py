@@ -72,7 +72,9 @@ def test_cfg0_q0_stage_parity_vs_reference():
     for g, seed, hkey, headkey in ((g1, 0, "hist1", "q1_head"), (g2, 1, "hist2", "q2_head")):
         res = rg.extract_basis(g, rg.ExtractionConfig.fixed_rank(cfg.k, seed, 0))
         ob = orc.fixed_rank_basis(g, cfg.k, 0, seed)
-        assert np.array_equal(ob.q[:32], gd[headkey])  # oracle == reference here
+        # the oracle reproduces the reference exactly only on the same BLAS build;
+        # across hosts the noise columns (cond ~ 1e9) move at ~1e-8
+        assert np.max(np.abs(ob.q[:32, :cfg.s] - gd[headkey][:, :cfg.s])) <= 1e-13
         check_basis(g, res, ob, cfg.s)
         assert abs(res.residual_history[1] - gd[hkey][1]) <= 1e-6 * gd[hkey][0]
         # leading signal columns agree entrywise (same positive-R phase)
