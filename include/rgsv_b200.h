@@ -48,6 +48,7 @@ extern "C" {
 #define RGSV_ST_CLASSIFY 0x8        /* overlapping zero classes (engine.py:179-180) */
 #define RGSV_ST_DEGENERATE 0x10     /* vanishing alpha/beta energy (analysis.py:58-59) */
 #define RGSV_ST_NOT_NORMALIZED 0x20 /* |sum p - 1| > 1e-10 (analysis.py:74-75) */
+#define RGSV_ST_OMEGA_SHORT 0x40    /* Omega generator ran out of raw draws (never expected) */
 
 const char* rgsv_version(void);
 
@@ -57,6 +58,17 @@ long long rgsv_launch_count(void);
 
 /* Compute capability (major*10+minor) of the current device, or -1. */
 int rgsv_device_cc(void);
+
+/* --- Omega: the reference's Gaussian test matrices, generated on the device
+ * Bit-identical to numpy 2.3.5 `default_rng(seed).standard_normal((n, k))`
+ * (rangefinder.py:101,112 / core.py:60-76): SeedSequence -> PCG64 ->
+ * 256-layer ziggurat, reproduced in parallel. Writes Omega^T: stream s's
+ * value Omega[i][j] goes to out[s * out_stride + j * ldo + i]. `seeds` is a
+ * DEVICE array of nstreams uint64 seeds (already masked to 64 bits). */
+size_t rgsv_omega_workspace_bytes(int nstreams, int64_t n, int k);
+int rgsv_omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double* out,
+                        int64_t ldo, int64_t out_stride, int* status, void* workspace,
+                        size_t workspace_bytes, void* stream);
 
 /* --- (1)-(3) range finder + projection for ONE matrix -------------------
  * Replaces rangefinder.extract_basis in fixed-rank mode (one block of
@@ -129,6 +141,9 @@ int rgsv_gemm_gtq(const double* a, int64_t lda, const double* b, int64_t ldb, do
                   size_t scratch_bytes, void* stream);
 int rgsv_chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv,
                   double* rinv, double* rdiag, int* status, void* stream);
+/* Debug: one Cholesky launch recording clock64() phase stamps into prof[]. */
+int rgsv_debug_chol_profile(const double* gram, int k, int kp, double* linv, long long* prof,
+                            int* status, void* stream);
 int rgsv_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
                void* workspace, size_t workspace_bytes, void* stream);
 

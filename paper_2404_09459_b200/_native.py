@@ -28,6 +28,7 @@ OK, ERR_DIMENSION, ERR_VALIDATION, ERR_RANK, ERR_CONVERGENCE, ERR_CUDA, ERR_WORK
     ERR_DEGENERATE = range(8)
 ST_CHOL, ST_NONFINITE, ST_JACOBI, ST_CLASSIFY, ST_DEGENERATE, ST_NOT_NORMALIZED = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
+ST_OMEGA_SHORT = 0x40
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -40,6 +41,8 @@ SIGNATURES = {
     "rgsv_version": (ctypes.c_char_p, []),
     "rgsv_device_cc": (_i32, []),
     "rgsv_launch_count": (ctypes.c_longlong, []),
+    "rgsv_omega_workspace_bytes": (_sz, [_i32, _i64, _i32]),
+    "rgsv_omega_generate": (_i32, [_p, _i32, _i64, _i32, _p, _i64, _i64, _p, _p, _sz, _p]),
     "rgsv_sketch_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "rgsv_sketch_project": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _i32, _i32, _p, _p, _i64, _p,
                                    _p, _p, _p, _sz, _p]),
@@ -54,6 +57,7 @@ SIGNATURES = {
     "rgsv_gemm_gx": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "rgsv_gemm_gtq": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "rgsv_chol_inv": (_i32, [_p, _i32, _i32, _i64, _p, _p, _p, _p, _p]),
+    "rgsv_debug_chol_profile": (_i32, [_p, _i32, _i32, _p, _p, _p, _p]),
     "rgsv_sumsq": (_i32, [_p, _i64, _i64, _i64, _p, _p, _sz, _p]),
 }
 

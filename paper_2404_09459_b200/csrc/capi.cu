@@ -130,6 +130,18 @@ int rgsv_device_cc(void) {
   return ma * 10 + mi;
 }
 
+size_t rgsv_omega_workspace_bytes(int nstreams, int64_t n, int k) {
+  return rgsv::omega_workspace_bytes(nstreams, n * (int64_t)k);
+}
+
+int rgsv_omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double* out,
+                        int64_t ldo, int64_t out_stride, int* status, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  if (nstreams < 1 || n < 1 || k < 1 || ldo < n) return RGSV_ERR_DIMENSION;
+  return rgsv::omega_generate(seeds, nstreams, n, k, out, ldo, out_stride, status, workspace,
+                              workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
 size_t rgsv_sketch_workspace_bytes(int64_t m, int64_t n, int k) {
   return sketch_layout(m, n, k).total;
 }
@@ -459,6 +471,11 @@ int rgsv_chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double*
                   double* rinv, double* rdiag, int* status, void* stream) {
   return chol_inv(gram, k, kp, shift_rows, linv, rinv, nullptr, rdiag, nullptr, status,
                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_debug_chol_profile(const double* gram, int k, int kp, double* linv, long long* prof,
+                            int* status, void* stream) {
+  return rgsv::chol_profile(gram, k, kp, linv, prof, status, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rgsv_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,

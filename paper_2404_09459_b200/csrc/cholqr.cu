@@ -118,9 +118,421 @@ __global__ void __launch_bounds__(512) k_chol_inv(const double* __restrict__ gra
   }
 }
 
+// Register-tiled variant for kp <= 128 (every range-finder Cholesky of the
+// fp64 configs and the stacked small QR up to l1 + l2 = 128): a DIM x DIM
+// thread grid, thread (ty, tx) owns the T x T tile A[ty*T.., tx*T..] of the
+// Schur complement and the same tile of X, the running unit-lower inverse
+// (registers, or shared memory when XS). Step j needs column j of A and row j
+// of X, which their owners publish into double-buffered shared vectors right
+// after their own update of step j-1: one __syncthreads per column. The
+// update itself is branch-free (select + FMA), so warps never diverge.
+template <int T, bool XS>
+__global__ void __launch_bounds__(256)
+    k_chol_reg(const double* __restrict__ gram, int k, int kp, int64_t shift_rows,
+               double* __restrict__ linv, double* __restrict__ rinv,
+               double* __restrict__ r_upper, double* __restrict__ rdiag,
+               double* __restrict__ rdiag_acc, int* __restrict__ status) {
+  __shared__ double colbuf[2][128];
+  __shared__ double rowbuf[2][128];
+  __shared__ double dbuf[128];
+  __shared__ double shift_s;
+  extern __shared__ double xsm[];  // XS: X as kp x (kp + 1)
+  const int DIM = kp / T;
+  const int tx = threadIdx.x % DIM, ty = threadIdx.x / DIM;
+  const int i0 = ty * T, l0 = tx * T;
+  const int ldx = kp + 1;
+  __shared__ double piv[128];  // D[j], written once by thread 0 at step j
+  double A[T][T], Xr[XS ? 1 : T][XS ? 1 : T];
+#define XREF(a, b) (XS ? xsm[(i0 + (a)) * ldx + l0 + (b)] : Xr[XS ? 0 : (a)][XS ? 0 : (b)])
+#pragma unroll
+  for (int a = 0; a < T; ++a) {
+#pragma unroll
+    for (int b = 0; b < T; ++b) {
+      const int i = i0 + a, l = l0 + b;
+      A[a][b] = (i < k && l < k && l <= i) ? gram[(int64_t)i * kp + l] : 0.0;
+      XREF(a, b) = (i == l) ? 1.0 : 0.0;
+    }
+  }
+  if (shift_rows > 0) {
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+      for (int b = 0; b < T; ++b)
+        if (i0 + a == l0 + b && i0 + a < k) dbuf[i0 + a] = A[a][b];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tr = 0.0;
+      for (int i = 0; i < k; ++i) tr += dbuf[i];
+      shift_s = 11.0 * ((double)shift_rows * k + (double)k * (k + 1)) * 0x1p-53 * tr;
+    }
+    __syncthreads();
+    const double sh = shift_s;
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+      for (int b = 0; b < T; ++b)
+        if (i0 + a == l0 + b && i0 + a < k) A[a][b] += sh;
+  }
+  if (tx == 0) {  // publish column 0
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+      if (i0 + a < k) colbuf[0][i0 + a] = A[a][0];
+  }
+  __syncthreads();
+  bool fail = false;
+  for (int j = 0; j < k; ++j) {
+    const int p = j & 1;
+    const double d = colbuf[p][j];
+    if (!(d > 0.0) || !isfinite(d)) {
+      fail = true;
+      break;
+    }
+    const double inv_d = 1.0 / d;
+    if (threadIdx.x == 0) piv[j] = d;
+    double cl[T], xr[T];
+#pragma unroll
+    for (int b = 0; b < T; ++b) {
+      const int l = l0 + b;
+      cl[b] = colbuf[p][l < 128 ? l : 0];
+      xr[b] = (l < j) ? rowbuf[p][l] : (l == j ? 1.0 : 0.0);  // X[j][l]
+    }
+#pragma unroll
+    for (int a = 0; a < T; ++a) {
+      const int i = i0 + a;
+      const bool live = (i > j) && (i < k);
+      const double li = live ? colbuf[p][i] * inv_d : 0.0;  // unit-lower L[i][j]
+#pragma unroll
+      for (int b = 0; b < T; ++b) {
+        const int l = l0 + b;
+        const double ta = (l > j && l <= i) ? cl[b] : 0.0;  // trailing Schur update
+        A[a][b] = fma(-li, ta, A[a][b]);
+        XREF(a, b) = fma(-li, xr[b], XREF(a, b));  // X[i][l] -= L[i][j] X[j][l], l <= j
+      }
+    }
+    const int jn = j + 1;
+    if (jn < k) {
+      if (jn >= l0 && jn < l0 + T) {
+#pragma unroll
+        for (int b = 0; b < T; ++b)
+          if (l0 + b == jn) {
+#pragma unroll
+            for (int a = 0; a < T; ++a)
+              if (i0 + a >= jn && i0 + a < k) colbuf[p ^ 1][i0 + a] = A[a][b];
+          }
+      }
+      if (jn >= i0 && jn < i0 + T) {
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+          if (i0 + a == jn) {
+#pragma unroll
+            for (int b = 0; b < T; ++b)
+              if (l0 + b < jn) rowbuf[p ^ 1][l0 + b] = XREF(a, b);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (threadIdx.x == 0) atomicOr(status, RGSV_ST_CHOL_BREAKDOWN);
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+      for (int b = 0; b < T; ++b) {
+        const int i = i0 + a, l = l0 + b;
+        linv[(int64_t)i * kp + l] = qnan;
+        if (rinv) rinv[(int64_t)l * kp + i] = qnan;
+      }
+    return;
+  }
+  __syncthreads();
+  double sr[T], rsc[T];
+#pragma unroll
+  for (int a = 0; a < T; ++a) {
+    sr[a] = (i0 + a < k) ? sqrt(piv[i0 + a]) : 1.0;
+    rsc[a] = (l0 + a < k) ? 1.0 / sqrt(piv[l0 + a]) : 1.0;
+  }
+#pragma unroll
+  for (int a = 0; a < T; ++a) {
+    const int i = i0 + a;
+    const double rsi = 1.0 / sr[a];
+#pragma unroll
+    for (int b = 0; b < T; ++b) {
+      const int l = l0 + b;
+      double v, ru;
+      if (i < k && l < k) {
+        v = (l <= i) ? XREF(a, b) * rsi : 0.0;                           // Linv = D^-1/2 X
+        ru = (l < i) ? A[a][b] * rsc[b] : (l == i ? sr[a] : 0.0);      // R[l][i] = L[i][l]
+        if (l == i) {
+          if (rdiag) rdiag[i] = sr[a];
+          if (rdiag_acc) rdiag_acc[i] *= sr[a];
+        }
+      } else {
+        v = (i == l) ? 1.0 : 0.0;
+        ru = v;
+      }
+      linv[(int64_t)i * kp + l] = v;
+      if (rinv) rinv[(int64_t)l * kp + i] = v;
+      if (r_upper) {
+        r_upper[(int64_t)l * kp + i] = ru;
+        if (l != i) r_upper[(int64_t)i * kp + l] = 0.0;
+      }
+    }
+  }
+#undef XREF
+}
+
+// Blocked variant (8-wide block columns) for kp <= 128. Per block column J:
+//   thread 0 factors the 8x8 diagonal block and inverts it in registers;
+//   all threads form the panel P = A[J+1:, J] L_JJ^-T and the block row
+//   XR = L_JJ^-1 W[J, :J+1] of the inverse; then the trailing Schur update
+//   A -= P P^T and the inverse update W[J+1:, :] -= P XR.
+// Three barriers per 8 columns; A, W (-> L^{-1}) and P live in shared memory.
+constexpr int kCholNB = 8;
+
+// DMMA fragment helpers for 8x8 tiles held in shared memory (row-major, ld).
+RGSV_DI void tile_mma_sub(double (&c)[2], const double* Arow8, int lda, const double* Brow8,
+                          int ldb, bool b_transposed) {
+  // c(8x8 frag) -= A(8x8) * B(8x8); A rows from Arow8, B given as rows of B
+  // (b_transposed = false: B[t][n] = Brow8[t*ldb + n]) or as rows of B^T
+  // (b_transposed = true: B[t][n] = Brow8[n*ldb + t]).
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 8; kk += 4) {
+    const double a = -Arow8[g * lda + kk + t];
+    const double bb = b_transposed ? Brow8[g * ldb + kk + t] : Brow8[(kk + t) * ldb + g];
+    dmma(c, a, bb);
+  }
+}
+
+// Blocked right-looking Cholesky + inverse for kp <= 128, 8-wide blocks.
+// Per block column J: thread 0 factors/inverts the 8x8 diagonal block in
+// registers; warps form the panel P = A[J+1:, J] L_JJ^-T and the block row
+// XR = L_JJ^-1 W[J, :J+1]; then every warp applies DMMA rank-8 updates to
+// its 8x8 tiles: A_IK -= P_I P_K^T (trailing Schur complement) and
+// W_IK -= P_I XR_K (inverse RHS). Three barriers per 8 columns.
+// Shared layout: A (kp x lda): lower triangle = Schur complement -> L,
+// strict upper = W^T (W -> L^{-1}, strictly lower part); Wd = diag(W).
+__global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gram, int k, int kp,
+                                                  int64_t shift_rows, double* __restrict__ linv,
+                                                  double* __restrict__ rinv,
+                                                  double* __restrict__ r_upper,
+                                                  double* __restrict__ rdiag,
+                                                  double* __restrict__ rdiag_acc,
+                                                  int* __restrict__ status,
+                                                  long long* __restrict__ prof = nullptr) {
+  extern __shared__ double sm[];
+  const int ld = kp + 4;
+#define PROF_MARK(slot) \
+  if (prof && threadIdx.x == 0) prof[(slot)] = clock64();
+  double* A = sm;
+  double* Wd = A + kp * ld;               // kp
+  double* P = Wd + kp;                    // kp x 8 panel (row-major, ld 8)
+  double* XR = P + kp * kCholNB;          // 8 x kp block row of L^{-1} (ld kp)
+  double* LJ = XR + kCholNB * kp;         // 8 x 8 L_JJ^{-1}
+  __shared__ int fail;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int kb = (k + kCholNB - 1) / kCholNB * kCholNB;
+  const int nb = kb / kCholNB;
+  for (int i = warp; i < kb; i += nwarp) {
+    for (int l = lane; l < kb; l += 32) {
+      double a = 0.0;
+      if (i < k && l < k) a = gram[(int64_t)i * kp + l];
+      else if (i == l) a = 1.0;
+      A[i * ld + l] = (l <= i) ? a : 0.0;
+    }
+    if (lane == 0) Wd[i] = 1.0;
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  if (shift_rows > 0) {
+    if (warp == 0) {
+      double tr = 0.0;
+      for (int i = lane; i < k; i += 32) tr += A[i * ld + i];
+      tr = warp_sum(tr);
+      const double sh = 11.0 * ((double)shift_rows * k + (double)k * (k + 1)) * 0x1p-53 * tr;
+      for (int i = lane; i < k; i += 32) A[i * ld + i] += sh;
+    }
+    __syncthreads();
+  }
+  PROF_MARK(0);
+  for (int Jb = 0; Jb < nb; ++Jb) {
+    const int J = Jb * kCholNB;
+    PROF_MARK(1 + 4 * Jb);
+    if (tid == 0) {
+      double L[kCholNB][kCholNB], X[kCholNB][kCholNB], rr[kCholNB];
+#pragma unroll
+      for (int j = 0; j < kCholNB; ++j) {
+        double d = A[(J + j) * ld + J + j];
+#pragma unroll
+        for (int t = 0; t < j; ++t) d = fma(-L[j][t], L[j][t], d);
+        if (!(d > 0.0) || !isfinite(d)) fail = 1;
+        const double r = rsqrt(d);
+        rr[j] = r;
+        L[j][j] = d * r;
+#pragma unroll
+        for (int i = j + 1; i < kCholNB; ++i) {
+          double v = A[(J + i) * ld + J + j];
+#pragma unroll
+          for (int t = 0; t < j; ++t) v = fma(-L[i][t], L[j][t], v);
+          L[i][j] = v * r;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kCholNB; ++j) {
+        X[j][j] = rr[j];
+#pragma unroll
+        for (int i = j + 1; i < kCholNB; ++i) {
+          double v = 0.0;
+#pragma unroll
+          for (int t = j; t < i; ++t) v = fma(L[i][t], X[t][j], v);
+          X[i][j] = -v * rr[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kCholNB; ++i)
+#pragma unroll
+        for (int j = 0; j < kCholNB; ++j) {
+          LJ[i * kCholNB + j] = (j <= i) ? X[i][j] : 0.0;
+          if (j <= i) A[(J + i) * ld + J + j] = L[i][j];
+        }
+    }
+    __syncthreads();
+    PROF_MARK(2 + 4 * Jb);
+    if (fail) break;
+    // panel tiles P_I = A_IJ L_JJ^-T (I > J) and XR_K = L_JJ^-1 W_JK (K <= J)
+    const int npanel = nb - 1 - Jb;
+    for (int task = warp; task < npanel + Jb + 1; task += nwarp) {
+      double c[2] = {0.0, 0.0};
+      if (task < npanel) {
+        const int I = (Jb + 1 + task) * kCholNB;
+        // P_I[g][n] = sum_t A[I+g][J+t] * LJ[n][t]
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4)
+          dmma(c, A[(I + g) * ld + J + kk + tq], LJ[g * kCholNB + kk + tq]);
+        P[(I + g) * kCholNB + 2 * tq] = c[0];
+        P[(I + g) * kCholNB + 2 * tq + 1] = c[1];
+      } else {
+        const int K = (task - npanel) * kCholNB;
+        // XR_K[r][n] = sum_t LJ[r][t] * W[J+t][K+n]  (W lower part in A^T, diag in Wd)
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4) {
+          const int row = J + kk + tq, col = K + g;
+          const double w = col < row ? A[col * ld + row] : (col == row ? Wd[row] : 0.0);
+          dmma(c, LJ[g * kCholNB + kk + tq], w);
+        }
+        XR[g * kp + K + 2 * tq] = c[0];
+        XR[g * kp + K + 2 * tq + 1] = c[1];
+      }
+    }
+    __syncthreads();
+    PROF_MARK(3 + 4 * Jb);
+    // DMMA rank-8 updates: trailing tiles (I >= K > J) and inverse tiles (I > J >= K)
+    const int ntrail = npanel * (npanel + 1) / 2;
+    const int ninv = npanel * (Jb + 1);
+    for (int task = warp; task < ntrail + ninv + npanel; task += nwarp) {
+      if (task < ntrail) {
+        // decode (I, K) with K <= I over the npanel x npanel lower triangle
+        int ii = 0, rem = task;
+        while (rem > ii) { rem -= ii + 1; ++ii; }
+        const int I = (Jb + 1 + ii) * kCholNB, K = (Jb + 1 + rem) * kCholNB;
+        double c[2];
+        const int r0 = I + g, c0 = K + 2 * tq;
+        c[0] = A[r0 * ld + c0];
+        c[1] = A[r0 * ld + c0 + 1];
+        tile_mma_sub(c, P + I * kCholNB, kCholNB, P + K * kCholNB, kCholNB, true);
+        if (I != K || c0 <= r0) A[r0 * ld + c0] = c[0];
+        if (I != K || c0 + 1 <= r0) A[r0 * ld + c0 + 1] = c[1];
+      } else if (task < ntrail + ninv) {
+        const int v = task - ntrail;
+        const int I = (Jb + 1 + v / (Jb + 1)) * kCholNB, K = (v % (Jb + 1)) * kCholNB;
+        // W_IK -= P_I XR_K; W_IK[g][n] lives at A[(K+n)*ld + I+g]
+        double c[2];
+        const int r0 = I + g, n0 = K + 2 * tq;
+        c[0] = A[n0 * ld + r0];
+        c[1] = A[(n0 + 1) * ld + r0];
+        tile_mma_sub(c, P + I * kCholNB, kCholNB, XR + K, kp, false);
+        A[n0 * ld + r0] = c[0];
+        A[(n0 + 1) * ld + r0] = c[1];
+      } else {
+        // finalize block column J of L for panel block I
+        const int I = (Jb + 1 + (task - ntrail - ninv)) * kCholNB;
+        for (int e = lane; e < 64; e += 32)
+          A[(I + (e >> 3)) * ld + J + (e & 7)] = P[(I + (e >> 3)) * kCholNB + (e & 7)];
+      }
+    }
+    // finalize block row J of L^{-1}
+    for (int e = tid; e < kCholNB * (J + kCholNB); e += nt) {
+      const int r = e / (J + kCholNB), c = e % (J + kCholNB), row = J + r;
+      if (c < row) A[c * ld + row] = XR[r * kp + c];
+      else if (c == row) Wd[row] = XR[r * kp + c];
+    }
+    __syncthreads();
+    PROF_MARK(4 + 4 * Jb);
+  }
+#undef PROF_MARK
+  if (fail) {
+    if (tid == 0) atomicOr(status, RGSV_ST_CHOL_BREAKDOWN);
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    for (int e = tid; e < kp * kp; e += nt) {
+      linv[e] = qnan;
+      if (rinv) rinv[e] = qnan;
+    }
+    return;
+  }
+  for (int i = warp; i < kp; i += nwarp) {
+    for (int l = lane; l < kp; l += 32) {
+      double v, ru;
+      if (i < k && l < k) {
+        v = (l < i) ? A[l * ld + i] : (l == i ? Wd[i] : 0.0);
+        ru = (l <= i) ? A[i * ld + l] : 0.0;
+      } else {
+        v = (i == l) ? 1.0 : 0.0;
+        ru = v;
+      }
+      linv[(int64_t)i * kp + l] = v;
+      if (rinv) rinv[(int64_t)l * kp + i] = v;
+      if (r_upper) r_upper[(int64_t)l * kp + i] = ru;
+    }
+  }
+  for (int i = tid; i < k; i += nt) {
+    const double si = A[i * ld + i];
+    if (rdiag) rdiag[i] = si;
+    if (rdiag_acc) rdiag_acc[i] *= si;
+  }
+}
+
+int chol_profile(const double* gram, int k, int kp, double* linv, long long* prof,
+                 int* status, cudaStream_t st) {
+  if (kp > 128) return RGSV_ERR_DIMENSION;
+  const size_t bytes = ((size_t)kp * (kp + 4) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
+  cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(((size_t)128 * 132 + 128 + 2 * 128 * kCholNB + 64) * sizeof(double)));
+  k_chol_blk<<<1, 256, bytes, st>>>(gram, k, kp, 0, linv, nullptr, nullptr, nullptr, nullptr,
+                                    status, prof);
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
 int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
              double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st) {
   if (k <= 0 || kp < k || kp % 16 != 0 || kp > 512) return RGSV_ERR_DIMENSION;
+  if (kp <= 128) {
+    const size_t bytes = ((size_t)kp * (kp + 4) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
+    static bool attr_blk = false;
+    if (!attr_blk) {
+      if (cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(((size_t)128 * 132 + 128 + 2 * 128 * kCholNB + 64) *
+                                     sizeof(double))) != cudaSuccess)
+        return RGSV_ERR_CUDA;
+      attr_blk = true;
+    }
+    k_chol_blk<<<1, 256, bytes, st>>>(gram, k, kp, shift_rows, linv, rinv, r_upper, rdiag,
+                                      rdiag_acc, status);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+  }
   const size_t wbytes = (size_t)kp * (kp + 1) * sizeof(double);
   if (wbytes <= 200 * 1024) {
     static bool attr = false;

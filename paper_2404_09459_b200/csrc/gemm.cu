@@ -277,18 +277,43 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
   }
 }
 
-// out[r][c] = sum_{s < S} part[s][r][c] for r < rows, c < cols (fixed order).
-__global__ void k_reduce_splits(double* __restrict__ out, int64_t ld, const double* __restrict__ part,
-                                int64_t part_stride, int S, int rows, int cols) {
+// out[r][c] = sum_{s < S} part[s][r][c] for r < rows, c < cols. A block
+// handles 32 consecutive entries with 8 warps splitting the S partials
+// (coalesced 256-byte rows per warp), then folds the 8 warp sums in a fixed
+// order: bitwise deterministic.
+__global__ void __launch_bounds__(256) k_reduce_splits(double* __restrict__ out, int64_t ld,
+                                                       const double* __restrict__ part,
+                                                       int64_t part_stride, int S, int rows,
+                                                       int cols) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t total = (int64_t)rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = static_cast<int>(e / cols), c = static_cast<int>(e % cols);
-    const double* p = part + (int64_t)r * ld + c;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
+    const int64_t e = base + lane;
     double acc = 0.0;
-    for (int s = 0; s < S; ++s) acc += p[s * part_stride];
-    out[(int64_t)r * ld + c] = acc;
+    int64_t off = 0;
+    if (e < total) {
+      off = (e / cols) * ld + (e % cols);
+      const double* p = part + off;
+#pragma unroll 4
+      for (int s = grp; s < S; s += 8) acc += p[(int64_t)s * part_stride];
+    }
+    red[grp][lane] = acc;
+    __syncthreads();
+    if (grp == 0 && e < total) {
+      double t = 0.0;
+#pragma unroll
+      for (int g2 = 0; g2 < 8; ++g2) t += red[g2][lane];
+      out[off] = t;
+    }
+    __syncthreads();
   }
+}
+
+static int reduce_blocks(int64_t total) {
+  int64_t b = (total + 31) / 32;
+  if (b > 8 * kSMs) b = 8 * kSMs;
+  return b < 1 ? 1 : (int)b;
 }
 
 // -------------------------------------------------------------- host side
@@ -368,9 +393,7 @@ int run_gx(const GemmArgs& a, cudaStream_t st) {
   note_launch();
   if (S > 0) {
     const int rows = (int)(a.M - part_row0);
-    const int64_t total = (int64_t)rows * a.N;
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+    const int blocks = reduce_blocks((int64_t)rows * a.N);
     k_reduce_splits<<<blocks, 256, 0, st>>>(a.C + (int64_t)part_row0 * a.ldc, a.ldc, a.scratch,
                                             part_stride, S, rows, (int)a.N);
     note_launch();
@@ -420,9 +443,7 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
                                                  (int)a.M, (int)a.N, d);
   note_launch();
   if (S > 0) {
-    const int64_t total = (int64_t)a.M * a.N;
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+    const int blocks = reduce_blocks((int64_t)a.M * a.N);
     k_reduce_splits<<<blocks, 256, 0, st>>>(a.C, a.ldc, a.scratch, part_stride, S, (int)a.M,
                                             (int)a.N);
     note_launch();

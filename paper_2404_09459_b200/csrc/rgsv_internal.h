@@ -35,6 +35,14 @@ int gemm_gtq(const GemmArgs& a, cudaStream_t st);
 int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
              double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st);
 
+int chol_profile(const double* gram, int k, int kp, double* linv, long long* prof, int* status,
+                 cudaStream_t st);
+
+size_t omega_workspace_bytes(int nstreams, int64_t nvals);
+int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double* out,
+                   int64_t ldo, int64_t out_stride, int* status, void* ws, size_t ws_bytes,
+                   cudaStream_t st);
+
 struct Workspace {
   char* base;
   size_t bytes;

@@ -105,10 +105,31 @@ def to_device(a, name: str = "matrix") -> DevMatrix:
     return DevMatrix(dev, rows, cols)
 
 
-def omega_host(n: int, k: int, seed: int) -> np.ndarray:
-    """The reference's Gaussian test matrix: one block of width k drawn from
-    default_rng(seed & (2^64 - 1)) (rangefinder.py:101,112)."""
-    return np.random.default_rng(int(seed) & SEED_MASK).standard_normal((n, k))
+def seed_word(seed: int) -> int:
+    """The reference's seed convention, seed & (2^64 - 1) (rangefinder.py:101),
+    as the two's-complement int64 a torch tensor can hold."""
+    v = int(seed) & SEED_MASK
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+def omega_device(n: int, k: int, seeds, ldo: int | None = None) -> torch.Tensor:
+    """Omega^T blocks (len(seeds) x kp x ldo) drawn on the device, bit-identical
+    to default_rng(seed).standard_normal((n, k)) (rgsv_omega_generate)."""
+    require_device()
+    kp = ceil16(k)
+    ldo = ldo or ceil16(n)
+    seeds = list(seeds)
+    ns = len(seeds)
+    out = torch.zeros((ns, kp, ldo), dtype=F64, device="cuda")
+    sd = torch.tensor([seed_word(x) for x in seeds], dtype=torch.int64).cuda()
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nb = int(lib().rgsv_omega_workspace_bytes(ns, n, k))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    check(lib().rgsv_omega_generate(vp(sd), ns, n, k, vp(out), ldo, kp * ldo, vp(status), vp(ws),
+                                    nb, sp(torch.cuda.current_stream())), "rgsv_omega_generate")
+    if int(status.item()) & _native.ST_OMEGA_SHORT:
+        raise RuntimeError("Omega generator exhausted its draw margin")
+    return out
 
 
 # ----------------------------------------------------------------- results
@@ -166,14 +187,25 @@ class SketchPlan:
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
         self.q = torch.zeros((m, self.kp), dtype=F64, device="cuda")
         self.b = torch.zeros((self.kp, self.ldb), dtype=F64, device="cuda")
-        self.om_host = torch.zeros((self.kp, self.ldb), dtype=F64, pin_memory=True)
         self.om_dev = torch.zeros((self.kp, self.ldb), dtype=F64, device="cuda")
+        self.seed_host = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        self.seed_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.om_ws_bytes = int(L.rgsv_omega_workspace_bytes(1, n, k))
+        self.om_ws = torch.empty(self.om_ws_bytes, dtype=torch.uint8, device="cuda")
 
-    def upload_omega(self, seed: int, stream) -> None:
-        om = omega_host(self.n, self.k, seed)
-        self.om_host[: self.k, : self.n].copy_(torch.from_numpy(om.T))
+    def set_seed(self, seed: int) -> None:
+        """Host side of Omega: only the 8-byte seed (the H2D copy and the
+        generation are part of the launch sequence / CUDA graph)."""
+        self.seed_host[0] = seed_word(seed)
+
+    def enqueue_omega(self, status: torch.Tensor, stream) -> None:
+        """Omega^T for this chain, generated on the device (rgsv_omega_generate)."""
         with torch.cuda.stream(stream):
-            self.om_dev.copy_(self.om_host, non_blocking=True)
+            self.seed_dev.copy_(self.seed_host, non_blocking=True)
+        rc = lib().rgsv_omega_generate(vp(self.seed_dev), 1, self.n, self.k, vp(self.om_dev),
+                                       self.ldb, 0, vp(status), vp(self.om_ws), self.om_ws_bytes,
+                                       sp(stream))
+        check(rc, "rgsv_omega_generate")
 
     def launch(self, g: DevMatrix, q_iters: int, stats: torch.Tensor, rdiag: torch.Tensor,
                status: torch.Tensor, stream) -> None:
@@ -195,16 +227,21 @@ class PairPlan:
         self.small_ws = torch.empty(self.small_bytes, dtype=torch.uint8, device="cuda")
         self.pk = _Packed(n, k1, k2)
         self.side = torch.cuda.Stream()
+        self.graph = None
+        self.graph_key = None
+        self.last_key = None
 
-    def run(self, g1: DevMatrix, g2: DevMatrix, seed: int, q_iters: int, classify_tol: float,
-            sync: bool = True):
+    def enqueue(self, g1: DevMatrix, g2: DevMatrix, q_iters: int, classify_tol: float) -> None:
+        """Every device operation of one pair, on the current stream (G1
+        chain, small GSVD, comparative kernel, packed D2H) and the side
+        stream (G2 chain). Capturable as one CUDA graph."""
         L = lib()
         main = torch.cuda.current_stream()
         pk = self.pk
         pk.d("status").zero_()
-        self.s1.upload_omega(seed, main)
-        self.s2.upload_omega(seed + 1, main)  # engine.py:252-253
         self.side.wait_stream(main)
+        self.s1.enqueue_omega(pk.d("status"), main)
+        self.s2.enqueue_omega(pk.d("status"), self.side)
         self.s1.launch(g1, q_iters, pk.d("stats1"), pk.d("rdiag1"), pk.d("status"), main)
         self.s2.launch(g2, q_iters, pk.d("stats2"), pk.d("rdiag2"), pk.d("status"), self.side)
         main.wait_stream(self.side)
@@ -220,9 +257,35 @@ class PairPlan:
                                 vp(pk.d("status")), sp(main))
         check(rc, "rgsv_comparative")
         pk.host.copy_(pk.dev, non_blocking=True)
+
+    def run(self, g1: DevMatrix, g2: DevMatrix, seed: int, q_iters: int, classify_tol: float,
+            sync: bool = True):
+        """One pair: stage the two seeds (reference convention: seed for G1,
+        seed + 1 for G2, engine.py:252-253), then replay the captured CUDA
+        graph when the device buffers are the captured ones, otherwise launch
+        eagerly (and capture on the second sighting)."""
+        self.s1.set_seed(seed)
+        self.s2.set_seed(int(seed) + 1)
+        key = (g1.t.data_ptr(), g1.ld, g1.rows, g2.t.data_ptr(), g2.ld, g2.rows, int(q_iters),
+               float(classify_tol))
+        if self.graph is not None and self.graph_key == key:
+            self.graph.replay()
+        elif USE_GRAPHS and self.last_key == key:
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self.enqueue(g1, g2, q_iters, classify_tol)
+            self.graph, self.graph_key = graph, key
+            graph.replay()
+        else:
+            self.enqueue(g1, g2, q_iters, classify_tol)
+        self.last_key = key
         if sync:
-            main.synchronize()
-        return pk
+            torch.cuda.current_stream().synchronize()
+        return self.pk
+
+
+USE_GRAPHS = True
 
 
 _PLANS: dict = {}
@@ -254,5 +317,5 @@ def device_sumsq(g: DevMatrix) -> float:
     return float(out.item())
 
 
-__all__ = ["DevMatrix", "to_device", "pair_plan", "PairPlan", "SketchPlan", "omega_host",
+__all__ = ["DevMatrix", "to_device", "pair_plan", "PairPlan", "SketchPlan", "omega_device",
            "residual_history", "device_sumsq", "ceil16", "_native"]

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import device as _dev
-from ._native import ST_CHOL, ST_CLASSIFY, ST_JACOBI
+from ._native import ST_CHOL, ST_CLASSIFY, ST_JACOBI, ST_OMEGA_SHORT
 from .errors import (
     ConvergenceError,
     DimensionError,
@@ -250,6 +250,8 @@ def unpack(pk, plan, opts: GsvOptions) -> DeviceRun:
         hist = _dev.residual_history(float(gf2), float(energy))
         tol = opts.extraction.tol if opts.extraction.tol is not None else 1e-10 * hist[0]
         bases.append(BasisResult(None, hist, hist[-1] < tol, 1, [k]))
+    if status & ST_OMEGA_SHORT:
+        raise RuntimeError("device Omega generator exhausted its draw margin")
     if status & ST_CHOL:
         raise RankDeficiencyError("CholeskyQR breakdown: a sketch or the stacked pair is "
                                   "numerically rank deficient")

@@ -103,7 +103,8 @@ def extract_basis(g, cfg: ExtractionConfig | None = None, *, device_result: bool
     rdiag = torch.zeros(max(width, 1), dtype=torch.float64, device="cuda")
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     st = torch.cuda.current_stream()
-    plan.upload_omega(cfg.seed, st)
+    plan.set_seed(cfg.seed)
+    plan.enqueue_omega(status, st)
     plan.launch(a, cfg.power_iters, stats, rdiag, status, st)
     gf2, energy = (float(x) for x in stats.cpu().tolist())
     code = int(status.item())
