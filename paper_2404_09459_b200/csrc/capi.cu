@@ -23,6 +23,9 @@ int launch_comparative(const double* sv1, const int* nsv, const double* sv2, int
 int launch_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
                  double* part, int max_parts, cudaStream_t st);
 int launch_sum(const double* part, int n, double* out, cudaStream_t st);
+size_t householder_small_smem(int l);
+int launch_householder_small(const double* b1, int64_t ld1, int l1, const double* b2, int64_t ld2,
+                             int l2, double* q, int64_t ldq, double* gwork, cudaStream_t st);
 
 static std::atomic<long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -318,7 +321,14 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
   double* Q = nullptr;
   int64_t ldq = 0;
   int r = 0;
-  if (l <= n) {
+  if (l <= n && l <= 512) {
+    // wide S: Householder Q of the leading l x l block (= Q of S, see
+    // k_householder_small), one CTA (shared memory, or L2-resident scratch)
+    Q = T;
+    ldq = lp;
+    if (int e = launch_householder_small(b1, ldb1, l1, b2, ldb2, l2, Q, ldq, S, st)) return e;
+    r = l;
+  } else if (l <= n) {
     // S = [B1; B2] (l x n, wide). S^T = P T (CholQR3 on S^T), so
     // range(S) = range(T^T) and the Q of qr(S) is the Q of qr(T^T).
     if (int e = launch_stack(S, lds, b1, ldb1, l1, b2, ldb2, l2, (int)lp, n, st)) return e;

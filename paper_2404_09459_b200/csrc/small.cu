@@ -60,14 +60,23 @@ RGSV_DI int rr_index(int p, int round, int nplayers) {
 constexpr int kJacobiMaxVec = 2048;
 
 __global__ void __launch_bounds__(1024) k_jacobi_rows(JacobiJob j0, JacobiJob j1, int max_sweeps,
-                                                       int* __restrict__ status) {
-  const JacobiJob J = blockIdx.x == 0 ? j0 : j1;
+                                                       int* __restrict__ status, int use_smem) {
+  JacobiJob J = blockIdx.x == 0 ? j0 : j1;
   __shared__ double nrm[kJacobiMaxVec];
+  extern __shared__ double jsm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int nout = J.nv < J.len ? J.nv : J.len;
   if (J.nv <= 0 || J.len <= 0) {
     if (tid == 0) *J.nsv_out = 0;
     return;
+  }
+  if (use_smem) {  // stage the vectors in shared memory (ld len + 1)
+    const int lds = J.len + 1;
+    for (int i = warp; i < J.nv; i += nwarps)
+      for (int e = lane; e < J.len; e += 32) jsm[i * lds + e] = J.v[(int64_t)i * J.ld + e];
+    J.v = jsm;
+    J.ld = lds;
+    __syncthreads();
   }
   const int nve = J.nv + (J.nv & 1);
   const double tol = fmax(1e-15, sqrt((double)J.len) * 2.220446049250313e-16);
@@ -127,6 +136,147 @@ __global__ void __launch_bounds__(1024) k_jacobi_rows(JacobiJob j0, JacobiJob j1
     if (rank < nout) J.sv_out[rank] = x;
   }
   if (tid == 0) *J.nsv_out = nout;
+}
+
+// ------------------------------------------------------ Householder QR
+// Q of the Householder QR of the l x l leading block T = S[:, :l] of the
+// stacked S = [B1; B2] (l <= n). LAPACK dgeqrf/dorgqr (numpy.linalg.qr,
+// core.py:87, called by engine.py:257) process columns left to right, so for
+// a wide S the Q factor depends on the first l columns only: Q(S) = Q(T).
+// One CTA, T in shared memory; dgeqr2 (reflector per column, H = I - tau v
+// v^T with v[0] = 1) then dorg2r (backward accumulation of Q = H0 .. H_{l-1}).
+// Column signs of Q may differ from the reference's phase fix
+// (core.py:88-95); singular values of its row blocks do not depend on them.
+template <bool SMEM>
+__global__ void __launch_bounds__(512) k_householder_small(const double* __restrict__ b1,
+                                                           int64_t ld1, int l1,
+                                                           const double* __restrict__ b2,
+                                                           int64_t ld2, int l2,
+                                                           double* __restrict__ q, int64_t ldq,
+                                                           double* __restrict__ gwork) {
+  extern __shared__ double smh[];
+  const int l = l1 + l2;
+  const int lda = l + 1;
+  double* A = SMEM ? smh : gwork;  // l x lda: T -> R + reflectors -> Q (in place)
+  __shared__ double w[512];
+  __shared__ double tau[512];
+  __shared__ double s_beta, s_scale, s_tau;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarp = nt >> 5;
+  // 2-D thread view for element loops: row stride nwarp, column stride 32
+  for (int i = warp; i < l; i += nwarp) {
+    const double* src = (i < l1) ? b1 + (int64_t)i * ld1 : b2 + (int64_t)(i - l1) * ld2;
+    for (int j = lane; j < l; j += 32) A[i * lda + j] = src[j];
+  }
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    // reflector from A[j:, j] (dlarfg)
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < l; i += 32) ss = fma(A[i * lda + j], A[i * lda + j], ss);
+      ss = warp_sum(ss);
+      if (lane == 0) {
+        const double alpha = A[j * lda + j];
+        if (ss == 0.0) {
+          s_tau = 0.0;
+          s_scale = 0.0;
+          s_beta = alpha;
+        } else {
+          const double nrm = sqrt(fma(alpha, alpha, ss));
+          const double beta = alpha >= 0.0 ? -nrm : nrm;
+          s_tau = (beta - alpha) / beta;
+          s_scale = 1.0 / (alpha - beta);
+          s_beta = beta;
+        }
+        tau[j] = s_tau;
+      }
+    }
+    __syncthreads();
+    const double tj = s_tau, sc = s_scale;
+    if (warp == 0) {
+      for (int i = j + 1 + lane; i < l; i += 32) A[i * lda + j] *= sc;  // v, v[0] = 1 implicit
+      if (lane == 0) A[j * lda + j] = s_beta;
+    }
+    __syncthreads();
+    if (tj != 0.0) {
+      // w[c] = tau v^T A[j:, c], c > j ; one warp per column, lanes over rows
+      for (int c = j + 1 + warp; c < l; c += nwarp) {
+        double acc0 = (lane == 0) ? A[j * lda + c] : 0.0, acc1 = 0.0;
+        int i = j + 1 + lane;
+        for (; i + 32 < l; i += 64) {
+          acc0 = fma(A[i * lda + j], A[i * lda + c], acc0);
+          acc1 = fma(A[(i + 32) * lda + j], A[(i + 32) * lda + c], acc1);
+        }
+        if (i < l) acc0 = fma(A[i * lda + j], A[i * lda + c], acc0);
+        const double acc = warp_sum(acc0 + acc1);
+        if (lane == 0) w[c] = acc * tj;
+      }
+      __syncthreads();
+      for (int i = j + warp; i < l; i += nwarp) {
+        const double vi = (i == j) ? 1.0 : A[i * lda + j];
+        for (int c = j + 1 + lane; c < l; c += 32) A[i * lda + c] = fma(-vi, w[c], A[i * lda + c]);
+      }
+      __syncthreads();
+    }
+  }
+  // dorg2r, in place: columns i+1.. already hold Q's columns; apply H(i)
+  // from the left to A[i:, i+1:], then turn column i into H(i) e_i.
+  for (int i = l - 1; i >= 0; --i) {
+    const double ti = tau[i];
+    if (i < l - 1 && ti != 0.0) {
+      for (int c = i + 1 + warp; c < l; c += nwarp) {
+        double acc0 = (lane == 0) ? A[i * lda + c] : 0.0, acc1 = 0.0;
+        int r = i + 1 + lane;
+        for (; r + 32 < l; r += 64) {
+          acc0 = fma(A[r * lda + i], A[r * lda + c], acc0);
+          acc1 = fma(A[(r + 32) * lda + i], A[(r + 32) * lda + c], acc1);
+        }
+        if (r < l) acc0 = fma(A[r * lda + i], A[r * lda + c], acc0);
+        const double acc = warp_sum(acc0 + acc1);
+        if (lane == 0) w[c] = acc * ti;
+      }
+      __syncthreads();
+      for (int r = i + warp; r < l; r += nwarp) {
+        const double vr = (r == i) ? 1.0 : A[r * lda + i];
+        for (int c = i + 1 + lane; c < l; c += 32) A[r * lda + c] = fma(-vr, w[c], A[r * lda + c]);
+      }
+      __syncthreads();
+    }
+    for (int r = tid; r < l; r += nt) {
+      if (r > i) A[r * lda + i] = -ti * A[r * lda + i];
+      else if (r == i) A[r * lda + i] = 1.0 - ti;
+      else A[r * lda + i] = 0.0;
+    }
+    __syncthreads();
+  }
+  for (int i = warp; i < l; i += nwarp)
+    for (int j = lane; j < l; j += 32) q[(int64_t)i * ldq + j] = A[i * lda + j];
+}
+
+size_t householder_small_smem(int l) {
+  return (size_t)l * (l + 1) * sizeof(double);
+}
+
+int launch_householder_small(const double* b1, int64_t ld1, int l1, const double* b2, int64_t ld2,
+                             int l2, double* q, int64_t ldq, double* gwork, cudaStream_t st) {
+  const int l = l1 + l2;
+  if (l > 512) return RGSV_ERR_DIMENSION;
+  const size_t smem = householder_small_smem(l);
+  if (smem <= 200 * 1024) {  // + 8 KB static stays under the 227 KB per-CTA limit
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(k_householder_small<true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+          cudaSuccess)
+        return RGSV_ERR_CUDA;
+      attr = true;
+    }
+    k_householder_small<true><<<1, 512, smem, st>>>(b1, ld1, l1, b2, ld2, l2, q, ldq, nullptr);
+  } else {
+    k_householder_small<false><<<1, 512, 0, st>>>(b1, ld1, l1, b2, ld2, l2, q, ldq, gwork);
+  }
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
 // ---------------------------------------------------------- comparative
@@ -350,7 +500,16 @@ int launch_jacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* 
   if (nv1 > kJacobiMaxVec || nv2 > kJacobiMaxVec) return RGSV_ERR_DIMENSION;
   JacobiJob a{v1, ld1, nv1, len1, sv1, nsv1};
   JacobiJob b{v2, ld2, nv2, len2, sv2, nsv2};
-  k_jacobi_rows<<<2, 1024, 0, st>>>(a, b, 60, status);
+  const size_t need = (size_t)max(nv1 * (len1 + 1), nv2 * (len2 + 1)) * sizeof(double);
+  const int use_smem = need <= 200 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_jacobi_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024) != cudaSuccess)
+      return RGSV_ERR_CUDA;
+    attr = true;
+  }
+  k_jacobi_rows<<<2, 1024, use_smem ? need : 0, st>>>(a, b, 60, status, use_smem);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
