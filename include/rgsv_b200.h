@@ -141,6 +141,10 @@ int rgsv_gemm_gtq(const double* a, int64_t lda, const double* b, int64_t ldb, do
                   size_t scratch_bytes, void* stream);
 int rgsv_chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv,
                   double* rinv, double* rdiag, int* status, void* stream);
+/* Debug: one small Householder QR launch recording clock64() phase stamps. */
+int rgsv_debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
+                                   int64_t ld2, int l2, double* q, int64_t ldq, long long* prof,
+                                   void* stream);
 /* Debug: one Cholesky launch recording clock64() phase stamps into prof[]. */
 int rgsv_debug_chol_profile(const double* gram, int k, int kp, double* linv, long long* prof,
                             int* status, void* stream);

@@ -17,7 +17,7 @@ import torch
 
 from . import device as _dev
 from ._native import ST_DEGENERATE, ST_NOT_NORMALIZED, check, lib
-from .engine import GmpPair, GsvOptions, GsvSpectrum, run_device_pipeline
+from .engine import GmpPair, GsvOptions, GsvSpectrum, run_device_batch, run_device_pipeline
 from .errors import DegenerateSpectrumError, ValidationError
 
 QUARTER_PI = math.pi / 4
@@ -94,11 +94,7 @@ def shannon_entropy(p) -> float:
     return d
 
 
-def compare(pair: GmpPair, opts: GsvOptions | None = None) -> ComparativeReport:
-    """Spectrum + every comparison quantity, one device run
-    (analysis.py:82-102)."""
-    opts = opts or GsvOptions()
-    run = run_device_pipeline(pair, opts)
+def _report(run, opts: GsvOptions) -> ComparativeReport:
     if run.status & ST_DEGENERATE:
         raise DegenerateSpectrumError("spectrum has vanishing alpha- or beta-energy")
     if run.status & ST_NOT_NORMALIZED:
@@ -113,5 +109,20 @@ def compare(pair: GmpPair, opts: GsvOptions | None = None) -> ComparativeReport:
                              p2=run.p2, d1=run.d1, d2=run.d2, meta=meta)
 
 
+def compare_batch(pairs, opts: GsvOptions | None = None, seeds=None) -> list:
+    """compare over a batch of same-shape pairs run concurrently on the
+    device (throughput mode); equal to per-pair compare calls."""
+    opts = opts or GsvOptions()
+    return [_report(run, opts) for run in run_device_batch(pairs, opts, seeds)]
+
+
+def compare(pair: GmpPair, opts: GsvOptions | None = None) -> ComparativeReport:
+    """Spectrum + every comparison quantity, one device run
+    (analysis.py:82-102)."""
+    opts = opts or GsvOptions()
+    return _report(run_device_pipeline(pair, opts), opts)
+
+
 __all__ = ["ComparativeReport", "relative_significance", "angular_distances",
-           "eigenexpression_fractions", "shannon_entropy", "compare", "QUARTER_PI"]
+           "eigenexpression_fractions", "shannon_entropy", "compare", "compare_batch",
+           "QUARTER_PI"]

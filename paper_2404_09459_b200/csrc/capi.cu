@@ -24,6 +24,9 @@ int launch_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, doubl
                  double* part, int max_parts, cudaStream_t st);
 int launch_sum(const double* part, int n, double* out, cudaStream_t st);
 size_t householder_small_smem(int l);
+int debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
+                              int64_t ld2, int l2, double* q, int64_t ldq, long long* prof,
+                              cudaStream_t st);
 int launch_householder_small(const double* b1, int64_t ld1, int l1, const double* b2, int64_t ld2,
                              int l2, double* q, int64_t ldq, double* gwork, cudaStream_t st);
 
@@ -67,6 +70,7 @@ int make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t ou
 }
 
 static inline int64_t ceil16(int64_t x) { return (x + 15) / 16 * 16; }
+constexpr int kIntermediatePasses = 3;  // see the note in rgsv_sketch_project
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Upper bound of split-K partial storage for the GEMMs of one pipeline.
@@ -196,8 +200,13 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
   if (int e = launch_sum(ss, ss_units, stats, st)) return e;
   // (2) Q = qr(Y).q  (rangefinder.py:119)
   double* qres = nullptr;
+  // Every orthonormalisation is full shifted CholeskyQR3. (Fewer passes for
+  // the intermediate bases are exact in exact arithmetic -- each pass is a
+  // triangular right factor -- but measured on cfg0/cfg1 one pass inflates
+  // the last Y beyond what CholeskyQR3 resolves (full-span angle 8e-5,
+  // breakdowns) and two passes still miss the stage tolerances.)
   if (int e = cholqr3_tall(y, q_out, m, k, (int)kp, gram, linv, rd_ws, scratch, sb, status, &qres,
-                           st))
+                           st, q == 0 ? 3 : kIntermediatePasses))
     return e;
   for (int it = 0; it < q; ++it) {
     // Z^T = Q^T G, Qhat = qr(Z).q, Y = G Qhat, Q = qr(Y).q
@@ -217,7 +226,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
     if (int e = gemm_gtq(p, st)) return e;
     double* qt = nullptr;
     if (int e = cholqr3_wide(z, z2, n, ldn, k, (int)kp, gram, linv, rinv, rd_ws, scratch, sb,
-                             status, &qt, st))
+                             status, &qt, st, kIntermediatePasses))
       return e;
     GemmArgs y2 = s;
     y2.B = qt;
@@ -226,7 +235,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
     y2.ss_units = nullptr;
     if (int e = gemm_gx(y2, st)) return e;
     if (int e = cholqr3_tall(y, q_out, m, k, (int)kp, gram, linv, rd_ws, scratch, sb, status,
-                             &qres, st))
+                             &qres, st, it == q - 1 ? 3 : kIntermediatePasses))
       return e;
   }
   // (3) B = Q^T G (engine.py:255) and its energy (rangefinder.py:123)
@@ -481,6 +490,13 @@ int rgsv_chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double*
                   double* rinv, double* rdiag, int* status, void* stream) {
   return chol_inv(gram, k, kp, shift_rows, linv, rinv, nullptr, rdiag, nullptr, status,
                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
+                                   int64_t ld2, int l2, double* q, int64_t ldq, long long* prof,
+                                   void* stream) {
+  return rgsv::debug_householder_profile(b1, ld1, l1, b2, ld2, l2, q, ldq, prof,
+                                         reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rgsv_debug_chol_profile(const double* gram, int k, int kp, double* linv, long long* prof,

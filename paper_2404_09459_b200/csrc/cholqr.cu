@@ -12,6 +12,7 @@
 // one CTA (fused right-looking LDL^T + unit-lower inverse, one barrier per
 // column) writing L^{-1} so the TRSM is a GEMM.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "rgsv_internal.h"
@@ -510,7 +511,7 @@ int chol_profile(const double* gram, int k, int kp, double* linv, long long* pro
   const size_t bytes = ((size_t)kp * (kp + 4) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
   cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(((size_t)128 * 132 + 128 + 2 * 128 * kCholNB + 64) * sizeof(double)));
-  k_chol_blk<<<1, 256, bytes, st>>>(gram, k, kp, 0, linv, nullptr, nullptr, nullptr, nullptr,
+  k_chol_blk<<<1, 128, bytes, st>>>(gram, k, kp, 0, linv, nullptr, nullptr, nullptr, nullptr,
                                     status, prof);
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
@@ -528,7 +529,13 @@ int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv
         return RGSV_ERR_CUDA;
       attr_blk = true;
     }
-    k_chol_blk<<<1, 256, bytes, st>>>(gram, k, kp, shift_rows, linv, rinv, r_upper, rdiag,
+    // RGSV_CHOL_THREADS=128 keeps the CTA <= 16K registers so it can co-reside
+    // with a GEMM CTA of the other chain (slower alone: 41 vs 30 us at k = 60)
+    static int threads = [] {
+      const char* e = getenv("RGSV_CHOL_THREADS");
+      return (e && atoi(e) == 128) ? 128 : 256;
+    }();
+    k_chol_blk<<<1, threads, bytes, st>>>(gram, k, kp, shift_rows, linv, rinv, r_upper, rdiag,
                                       rdiag_acc, status);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
@@ -558,10 +565,10 @@ int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv
 
 int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram, double* linv,
                  double* rdiag, double* scratch, size_t scratch_bytes, int* status,
-                 double** q_out, cudaStream_t st) {
+                 double** q_out, cudaStream_t st, int passes) {
   double* src = y;
   double* dst = tmp;
-  for (int step = 0; step < 3; ++step) {
+  for (int step = 0; step < passes; ++step) {
     GemmArgs g;
     g.A = src;
     g.lda = kp;
@@ -603,10 +610,10 @@ int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram,
 
 int cholqr3_wide(double* b, double* tmp, int64_t n, int64_t ldn, int k, int kp, double* gram,
                  double* linv, double* rinv, double* rdiag, double* scratch, size_t scratch_bytes,
-                 int* status, double** qt_out, cudaStream_t st) {
+                 int* status, double** qt_out, cudaStream_t st, int passes) {
   double* src = b;
   double* dst = tmp;
-  for (int step = 0; step < 3; ++step) {
+  for (int step = 0; step < passes; ++step) {
     GemmArgs g;  // gram = B B^T (reduction over n)
     g.A = src;
     g.lda = ldn;

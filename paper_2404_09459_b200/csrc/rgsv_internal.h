@@ -58,14 +58,17 @@ struct Workspace {
 // Shifted CholeskyQR3 of a tall row-major m x kp block (k real columns,
 // zero padding). Input y is overwritten; the orthonormal factor is returned
 // in *q_out (one of y / tmp). rdiag (k) receives diag(R).
+// `passes` = 3 gives shifted CholeskyQR3 (orthonormal Q); 1 gives one shifted
+// pass, Y R1^{-1}: a triangular transform of Y, enough for intermediate bases
+// whose span (and nested leading spans) is all that is used downstream.
 int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram, double* linv,
                  double* rdiag, double* scratch, size_t scratch_bytes, int* status,
-                 double** q_out, cudaStream_t st);
+                 double** q_out, cudaStream_t st, int passes = 3);
 
 // Shifted CholeskyQR3 of Z = B^T where B is kp x n row-major (ld ldn):
 // returns Qhat^T (kp x n) in *qt_out (one of b / tmp).
 int cholqr3_wide(double* b, double* tmp, int64_t n, int64_t ldn, int k, int kp, double* gram,
                  double* linv, double* rinv, double* rdiag, double* scratch, size_t scratch_bytes,
-                 int* status, double** qt_out, cudaStream_t st);
+                 int* status, double** qt_out, cudaStream_t st, int passes = 3);
 
 }  // namespace rgsv

@@ -253,6 +253,184 @@ __global__ void __launch_bounds__(512) k_householder_small(const double* __restr
     for (int j = lane; j < l; j += 32) q[(int64_t)i * ldq + j] = A[i * lda + j];
 }
 
+// Register-resident variant for l <= 128: warp w owns columns c = w, w+16,
+// ... (CPW = 8 columns), lane r holds rows r, r+32, r+64, r+96 of each owned
+// column. Step j: the owner of column j forms the reflector (warp
+// reductions, no barrier) and publishes v and tau in shared memory; one
+// barrier; every warp applies H_j to its owned columns > j (interleaved warp
+// dot products). Q is then formed backwards from the stored reflectors
+// (dorg2r order), with the same column ownership.
+constexpr int kHhWarps = 16, kHhCPW = 8, kHhRPL = 4;  // 16 x 8 = 128 columns, 4 x 32 = 128 rows
+
+__global__ void __launch_bounds__(kHhWarps * 32) k_householder_reg(
+    const double* __restrict__ b1, int64_t ld1, int l1, const double* __restrict__ b2,
+    int64_t ld2, int l2, double* __restrict__ q, int64_t ldq, long long* __restrict__ prof) {
+  extern __shared__ double V[];  // reflectors: column j in V[j * 129 + r]; tau at V[128 * 129 + j]
+  double* tau_s = V + 128 * 129;
+  const int l = l1 + l2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a[kHhCPW][kHhRPL];
+#pragma unroll
+  for (int cc = 0; cc < kHhCPW; ++cc) {
+    const int c = warp + kHhWarps * cc;
+#pragma unroll
+    for (int rr = 0; rr < kHhRPL; ++rr) {
+      const int r = lane + 32 * rr;
+      double v = 0.0;
+      if (r < l && c < l) v = (r < l1) ? b1[(int64_t)r * ld1 + c] : b2[(int64_t)(r - l1) * ld2 + c];
+      a[cc][rr] = v;
+    }
+  }
+  // column j = slot * 16 + owner; `slot` is a compile-time index (unrolled)
+  // so the owned-column registers are never indexed dynamically
+#pragma unroll
+  for (int slot = 0; slot < kHhCPW; ++slot) {
+    for (int owner = 0; owner < kHhWarps; ++owner) {
+      const int j = slot * kHhWarps + owner;
+      if (j >= l) break;
+      if (prof && threadIdx.x == 0 && j < 8) prof[3 * j] = clock64();
+      if (warp == owner) {
+        double ss = 0.0, alpha = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < kHhRPL; ++rr) {
+          const int r = lane + 32 * rr;
+          const double xv = a[slot][rr];
+          if (r > j && r < l) ss = fma(xv, xv, ss);
+          if (r == j) alpha = xv;
+        }
+        ss = warp_sum(ss);
+        alpha = warp_sum(alpha);  // exactly one lane contributes
+        double tj, sc, beta;
+        if (ss == 0.0) {
+          tj = 0.0;
+          sc = 0.0;
+          beta = alpha;
+        } else {
+          const double nrm = sqrt(fma(alpha, alpha, ss));
+          beta = alpha >= 0.0 ? -nrm : nrm;
+          tj = (beta - alpha) / beta;
+          sc = 1.0 / (alpha - beta);
+        }
+#pragma unroll
+        for (int rr = 0; rr < kHhRPL; ++rr) {
+          const int r = lane + 32 * rr;
+          if (r > j && r < l) V[j * 129 + r] = a[slot][rr] * sc;
+          if (r == j) a[slot][rr] = beta;
+          else if (r > j) a[slot][rr] = 0.0;  // below-diagonal part now lives in V
+        }
+        if (lane == 0) {
+          V[j * 129 + j] = 1.0;
+          tau_s[j] = tj;
+        }
+      }
+      __syncthreads();
+      if (prof && threadIdx.x == 0 && j < 8) prof[3 * j + 1] = clock64();
+      const double tj = tau_s[j];
+      if (tj != 0.0) {
+        double v[kHhRPL];
+#pragma unroll
+        for (int rr = 0; rr < kHhRPL; ++rr) {
+          const int r = lane + 32 * rr;
+          v[rr] = (r >= j && r < l) ? V[j * 129 + r] : 0.0;
+        }
+        double d[kHhCPW];
+#pragma unroll
+        for (int cc = 0; cc < kHhCPW; ++cc) {
+          double acc = 0.0;
+#pragma unroll
+          for (int rr = 0; rr < kHhRPL; ++rr) acc = fma(v[rr], a[cc][rr], acc);
+          d[cc] = acc;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int cc = 0; cc < kHhCPW; ++cc) d[cc] += __shfl_xor_sync(0xffffffffu, d[cc], o);
+#pragma unroll
+        for (int cc = 0; cc < kHhCPW; ++cc) {
+          const int c = warp + kHhWarps * cc;
+          if (c > j) {
+            const double f = d[cc] * tj;
+#pragma unroll
+            for (int rr = 0; rr < kHhRPL; ++rr) a[cc][rr] = fma(-f, v[rr], a[cc][rr]);
+          }
+        }
+      }
+      if (prof && threadIdx.x == 0 && j < 8) prof[3 * j + 2] = clock64();
+    }
+  }
+  if (prof && threadIdx.x == 0) prof[30] = clock64();
+  // dorg2r: Q = H_0 ... H_{l-1} [I; 0]; walk i = l-1 .. 0 keeping Q[:, c] for
+  // c > i in the owned registers, then set column i to H_i e_i.
+#pragma unroll
+  for (int cc = 0; cc < kHhCPW; ++cc)
+#pragma unroll
+    for (int rr = 0; rr < kHhRPL; ++rr) a[cc][rr] = 0.0;
+#pragma unroll
+  for (int slot = kHhCPW - 1; slot >= 0; --slot) {
+    for (int owner = kHhWarps - 1; owner >= 0; --owner) {
+      const int i = slot * kHhWarps + owner;
+      if (i >= l) continue;
+      const double ti = tau_s[i];
+      double v[kHhRPL];
+#pragma unroll
+      for (int rr = 0; rr < kHhRPL; ++rr) {
+        const int r = lane + 32 * rr;
+        v[rr] = (r >= i && r < l) ? V[i * 129 + r] : 0.0;
+      }
+      if (ti != 0.0) {
+        double d[kHhCPW];
+#pragma unroll
+        for (int cc = 0; cc < kHhCPW; ++cc) {
+          double acc = 0.0;
+#pragma unroll
+          for (int rr = 0; rr < kHhRPL; ++rr) acc = fma(v[rr], a[cc][rr], acc);
+          d[cc] = acc;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int cc = 0; cc < kHhCPW; ++cc) d[cc] += __shfl_xor_sync(0xffffffffu, d[cc], o);
+#pragma unroll
+        for (int cc = 0; cc < kHhCPW; ++cc) {
+          const int c = warp + kHhWarps * cc;
+          if (c > i) {
+            const double f = d[cc] * ti;
+#pragma unroll
+            for (int rr = 0; rr < kHhRPL; ++rr) a[cc][rr] = fma(-f, v[rr], a[cc][rr]);
+          }
+        }
+      }
+      if (warp == owner) {  // column i := H_i e_i = e_i - tau v
+#pragma unroll
+        for (int rr = 0; rr < kHhRPL; ++rr) {
+          const int r = lane + 32 * rr;
+          a[slot][rr] = (r == i ? 1.0 : 0.0) - ti * v[rr];
+        }
+      }
+    }
+  }
+  if (prof && threadIdx.x == 0) prof[31] = clock64();
+#pragma unroll
+  for (int cc = 0; cc < kHhCPW; ++cc) {
+    const int c = warp + kHhWarps * cc;
+    if (c >= l) continue;
+#pragma unroll
+    for (int rr = 0; rr < kHhRPL; ++rr) {
+      const int r = lane + 32 * rr;
+      if (r < l) q[(int64_t)r * ldq + c] = a[cc][rr];
+    }
+  }
+}
+
+int debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
+                              int64_t ld2, int l2, double* q, int64_t ldq, long long* prof,
+                              cudaStream_t st) {
+  const size_t vbytes = (128 * 129 + 128) * sizeof(double);
+  cudaFuncSetAttribute(k_householder_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vbytes);
+  k_householder_reg<<<1, kHhWarps * 32, vbytes, st>>>(b1, ld1, l1, b2, ld2, l2, q, ldq, prof);
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
 size_t householder_small_smem(int l) {
   return (size_t)l * (l + 1) * sizeof(double);
 }
@@ -261,6 +439,20 @@ int launch_householder_small(const double* b1, int64_t ld1, int l1, const double
                              int l2, double* q, int64_t ldq, double* gwork, cudaStream_t st) {
   const int l = l1 + l2;
   if (l > 512) return RGSV_ERR_DIMENSION;
+  if (l <= kHhWarps * kHhCPW) {
+    const size_t vbytes = (128 * 129 + 128) * sizeof(double);
+    static bool attr_reg = false;
+    if (!attr_reg) {
+      if (cudaFuncSetAttribute(k_householder_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)vbytes) != cudaSuccess)
+        return RGSV_ERR_CUDA;
+      attr_reg = true;
+    }
+    k_householder_reg<<<1, kHhWarps * 32, vbytes, st>>>(b1, ld1, l1, b2, ld2, l2, q, ldq,
+                                                        nullptr);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+  }
   const size_t smem = householder_small_smem(l);
   if (smem <= 200 * 1024) {  // + 8 KB static stays under the 227 KB per-CTA limit
     static bool attr = false;

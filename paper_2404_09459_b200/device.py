@@ -230,6 +230,7 @@ class PairPlan:
         self.graph = None
         self.graph_key = None
         self.last_key = None
+        self.kernels_per_replay = 0
 
     def enqueue(self, g1: DevMatrix, g2: DevMatrix, q_iters: int, classify_tol: float) -> None:
         """Every device operation of one pair, on the current stream (G1
@@ -270,13 +271,19 @@ class PairPlan:
                float(classify_tol))
         if self.graph is not None and self.graph_key == key:
             self.graph.replay()
+            GRAPH_REPLAYS[0] += 1
+            GRAPH_REPLAYS[1] += self.kernels_per_replay
         elif USE_GRAPHS and self.last_key == key:
             torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
+            n0 = lib().rgsv_launch_count()
             with torch.cuda.graph(graph):
                 self.enqueue(g1, g2, q_iters, classify_tol)
+            self.kernels_per_replay = lib().rgsv_launch_count() - n0
             self.graph, self.graph_key = graph, key
             graph.replay()
+            GRAPH_REPLAYS[0] += 1
+            GRAPH_REPLAYS[1] += self.kernels_per_replay
         else:
             self.enqueue(g1, g2, q_iters, classify_tol)
         self.last_key = key
@@ -286,6 +293,75 @@ class PairPlan:
 
 
 USE_GRAPHS = True
+# [graph replays, library kernels executed by those replays] (the C-ABI
+# launch counter only sees launches issued while capturing)
+GRAPH_REPLAYS = [0, 0]
+
+
+class BatchPlan:
+    """B independent pairs of one shape processed concurrently: each pair's
+    two chains run on their own streams, all captured in ONE CUDA graph, so
+    the single-CTA latency steps of every chain overlap the other chains'
+    GEMMs (the throughput mode of compute_gsv_batch / compare_batch)."""
+
+    def __init__(self, B: int, m: int, p: int, n: int, k1: int, k2: int):
+        self.plans = [PairPlan(m, p, n, k1, k2) for _ in range(B)]
+        self.streams = [torch.cuda.Stream() for _ in range(B)]
+        self.graph = None
+        self.graph_key = None
+        self.last_key = None
+        self.kernels_per_replay = 0
+
+    def enqueue(self, pairs, q_iters: int, classify_tol: float) -> None:
+        cur = torch.cuda.current_stream()
+        for plan, st, (g1, g2) in zip(self.plans, self.streams, pairs):
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                plan.enqueue(g1, g2, q_iters, classify_tol)
+        for st in self.streams:
+            cur.wait_stream(st)
+
+    def run(self, pairs, seeds, q_iters: int, classify_tol: float, sync: bool = True):
+        for plan, seed in zip(self.plans, seeds):
+            plan.s1.set_seed(seed)
+            plan.s2.set_seed(int(seed) + 1)
+        key = tuple((g1.t.data_ptr(), g1.ld, g1.rows, g2.t.data_ptr(), g2.ld, g2.rows)
+                    for g1, g2 in pairs) + (int(q_iters), float(classify_tol))
+        if self.graph is not None and self.graph_key == key:
+            self.graph.replay()
+            GRAPH_REPLAYS[0] += 1
+            GRAPH_REPLAYS[1] += self.kernels_per_replay
+        elif USE_GRAPHS and self.last_key == key:
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            n0 = lib().rgsv_launch_count()
+            with torch.cuda.graph(graph):
+                self.enqueue(pairs, q_iters, classify_tol)
+            self.kernels_per_replay = lib().rgsv_launch_count() - n0
+            self.graph, self.graph_key = graph, key
+            graph.replay()
+            GRAPH_REPLAYS[0] += 1
+            GRAPH_REPLAYS[1] += self.kernels_per_replay
+        else:
+            self.enqueue(pairs, q_iters, classify_tol)
+        self.last_key = key
+        if sync:
+            torch.cuda.current_stream().synchronize()
+        return [plan.pk for plan in self.plans]
+
+
+_BATCH_PLANS: dict = {}
+
+
+def batch_plan(B: int, m: int, p: int, n: int, k1: int, k2: int) -> BatchPlan:
+    key = (torch.cuda.current_device(), B, m, p, n, k1, k2)
+    plan = _BATCH_PLANS.get(key)
+    if plan is None:
+        if len(_BATCH_PLANS) > 4:
+            _BATCH_PLANS.clear()
+        plan = BatchPlan(B, m, p, n, k1, k2)
+        _BATCH_PLANS[key] = plan
+    return plan
 
 
 _PLANS: dict = {}

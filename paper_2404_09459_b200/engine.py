@@ -271,6 +271,34 @@ def unpack(pk, plan, opts: GsvOptions) -> DeviceRun:
                      pk.h("sv1")[: nsv[0]].copy(), pk.h("sv2")[: nsv[1]].copy(), plan)
 
 
+def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
+    """B pairs of one shape, concurrently (device.BatchPlan). Pair b uses
+    extraction seed seeds[b] (default: opts.extraction.seed for every pair,
+    i.e. exactly compute_gsv(pair_b, opts) for each b)."""
+    pairs = list(pairs)
+    if not pairs:
+        return []
+    first = pairs[0]
+    for pr in pairs[1:]:
+        if (pr.m, pr.p, pr.n) != (first.m, first.p, first.n):
+            raise DimensionError("compute_gsv_batch needs pairs of one shape")
+    k1, k2 = _fixed_width(opts, first.m, first.p, first.n)
+    cfg = opts.extraction
+    seeds = [cfg.seed] * len(pairs) if seeds is None else list(seeds)
+    if len(seeds) != len(pairs):
+        raise DimensionError("one seed per pair")
+    plan = _dev.batch_plan(len(pairs), first.m, first.p, first.n, k1, k2)
+    pks = plan.run([(pr.g1, pr.g2) for pr in pairs], seeds, cfg.power_iters, opts.classify_tol)
+    return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]
+
+
+def compute_gsv_batch(pairs, opts: GsvOptions | None = None, seeds=None) -> list:
+    """compute_gsv over a batch of same-shape pairs, run concurrently on the
+    device (throughput mode); results equal per-pair compute_gsv calls."""
+    opts = opts or GsvOptions()
+    return [run.spectrum for run in run_device_batch(pairs, opts, seeds)]
+
+
 def compute_gsv(pair: GmpPair, opts: GsvOptions | None = None) -> GsvSpectrum:
     """GSV spectrum of a pair on the B200 (engine.py:264-275)."""
     opts = opts or GsvOptions()
@@ -296,5 +324,6 @@ def recover_gsvd(pair: GmpPair, opts: GsvOptions | None = None) -> GsvdFactors:
 
 
 __all__ = ["GmpPair", "GsvSpectrum", "GsvOptions", "GsvdFactors", "classify_spectrum",
-           "compute_gsv", "recover_gsvd", "run_device_pipeline", "RANDOMIZED", "DIRECT",
+           "compute_gsv", "compute_gsv_batch", "recover_gsvd", "run_device_pipeline",
+           "run_device_batch", "RANDOMIZED", "DIRECT",
            "dataclasses"]

@@ -216,3 +216,20 @@ def test_rank_check_and_reduced_qr():
                       compute_uv=False)
     assert abs(pair.stack_norm2 - s[0]) <= 1e-12 * s[0]
     assert abs(pair.stack_pinv_norm - 1 / s[-1]) <= 1e-10 / s[-1]
+
+
+def test_batch_equals_single():
+    cfg = CONFIGS["cfg0"]
+    pairs = [rg.GmpPair(*make_pair(cfg, data_seed=d, m=500, p=400)) for d in (1, 2, 3)]
+    opts = fixed_opts(cfg.k, cfg.q)
+    for _ in range(3):  # eager, capture, replay
+        reps = rg.compare_batch(pairs, opts, seeds=[5, 6, 7])
+    for pr, rep, seed in zip(pairs, reps, (5, 6, 7)):
+        single = rg.compare(pr, fixed_opts(cfg.k, cfg.q, seed))
+        assert np.array_equal(rep.spectrum.alphas, single.spectrum.alphas)
+        assert np.array_equal(rep.theta, single.theta) and rep.d1 == single.d1
+    run = rg.engine.run_device_batch(pairs, opts, seeds=[5, 6, 7])
+    ob = orc.fixed_rank_basis(make_pair(cfg, data_seed=2, m=500, p=400)[0], cfg.k, cfg.q, 6)
+    e_ref = orc.sum_sq(ob.b)
+    h = run[1].basis1.residual_history
+    assert abs(h[0] ** 2 - h[1] ** 2 - e_ref) <= 1e-12 * e_ref

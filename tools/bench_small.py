@@ -38,3 +38,18 @@ for (k, n) in ((30, 200), (60, 1000), (16, 64), (120, 4000)):
     s = sv1.cpu().numpy()
     print(f"small_gsvd k={k} n={n}: {e0.elapsed_time(e1) / 20 * 1e3:9.1f} us  status={int(ints[2])}"
           f"  sv1 range [{s.min():.17f}, {s.max():.17f}]")
+
+# phase stamps of one l = 60 Householder (owner phase / apply phase per column)
+k, n = 30, 200
+b1 = torch.from_numpy(np.random.default_rng(0).standard_normal((k, 208))).cuda()
+b2 = torch.from_numpy(np.random.default_rng(1).standard_normal((k, 208))).cuda()
+qq = torch.zeros((64, 64), dtype=torch.float64, device="cuda")
+prof = torch.zeros(64, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    L.rgsv_debug_householder_profile(dv.vp(b1), 208, k, dv.vp(b2), 208, k, dv.vp(qq), 64,
+                                     dv.vp(prof), st)
+torch.cuda.synchronize()
+p = prof.cpu().numpy()
+for j in range(6):
+    print(f"col {j}: owner {p[3*j+1]-p[3*j]} cycles, apply {p[3*j+2]-p[3*j+1]} cycles")
+print("factorization total", p[30] - p[0], "dorg2r", p[31] - p[30])
