@@ -185,7 +185,7 @@ __global__ void k_zig_seed(const uint64_t* __restrict__ seeds, int nstreams,
 
 __global__ void __launch_bounds__(kZigThreads) k_zig_attempt(
     const ZigStream* __restrict__ streams, int64_t P, double* __restrict__ val,
-    uint16_t* __restrict__ code, int* __restrict__ tile_nspec, uint16_t* __restrict__ tile_spec) {
+    uint16_t* __restrict__ code, int* __restrict__ tile_nspec, uint32_t* __restrict__ tile_spec) {
   const int s = blockIdx.y;
   const int64_t tile = blockIdx.x;
   const int64_t p0 = tile * kZigTile + threadIdx.x * kZigPerThread;
@@ -255,9 +255,14 @@ __global__ void __launch_bounds__(kZigThreads) k_zig_attempt(
   int base = 0;
   for (int w = 0; w < warp; ++w) base += wcount[w];
   int pos = base + incl - cnt;
-  uint16_t* ts = tile_spec + ((int64_t)s * gridDim.x + tile) * kZigTile;
+  uint32_t* ts = tile_spec + ((int64_t)s * gridDim.x + tile) * kZigTile;
   for (int q = 0; q < kZigPerThread; ++q)
-    if (specmask & (1u << q)) ts[pos++] = (uint16_t)(threadIdx.x * kZigPerThread + q);
+    if (specmask & (1u << q)) {
+      const int64_t pp = p0 + q;
+      const uint32_t c = pp < P ? cs[pp] : 1u;
+      ts[pos++] = (uint32_t)(threadIdx.x * kZigPerThread + q) | ((c & 0x3fffu) << 10) |
+                  ((c & 0x8000u) << 16);
+    }
   if (threadIdx.x == kZigThreads - 1) {
     int tot = 0;
     for (int w = 0; w < kZigThreads / 32; ++w) tot += wcount[w];
@@ -265,54 +270,78 @@ __global__ void __launch_bounds__(kZigThreads) k_zig_attempt(
   }
 }
 
-// One thread per stream: follow the attempt chain through the specials.
-// Marks swallowed positions (code |= 0x4000) and produces per-tile emit counts.
-__global__ void k_zig_walk(int nstreams, int ntiles, int64_t P, int64_t nvals,
-                           uint16_t* __restrict__ code, const int* __restrict__ tile_nspec,
-                           const uint16_t* __restrict__ tile_spec, int* __restrict__ tile_emit,
-                           int* __restrict__ status) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nstreams) return;
-  uint16_t* cs = code + (int64_t)s * P;
-  int* te = tile_emit + (int64_t)s * ntiles;
+// One warp per stream follows the attempt chain through the specials. The
+// tile's compact special records (offset | consumed << 10 | accepted << 31)
+// are staged in shared memory by the warp; lane 0 walks them. Positions that
+// emit nothing -- rejected starts and draws swallowed by multi-draw attempts
+// -- are recorded per tile as half-open intervals [a, b) of tile offsets;
+// the per-tile emit count is the tile length minus their total length.
+constexpr int kZigMaxIv = 64;  // intervals per tile (overflow -> status bit)
+
+__global__ void __launch_bounds__(32) k_zig_walk(int nstreams, int ntiles, int64_t P,
+                                                 int64_t nvals, const int* __restrict__ tile_nspec,
+                                                 const uint32_t* __restrict__ tile_spec,
+                                                 int* __restrict__ tile_emit,
+                                                 int* __restrict__ tile_niv,
+                                                 uint32_t* __restrict__ tile_iv,
+                                                 int* __restrict__ status) {
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x;
+  __shared__ uint32_t rec[kZigTile];
+  __shared__ uint32_t iv[kZigMaxIv];
   int64_t covered = 0;  // positions [0, covered) decided by the chain so far
   int64_t total = 0;
+  bool overflow = false;
   for (int t = 0; t < ntiles; ++t) {
     const int64_t t0 = (int64_t)t * kZigTile;
     const int64_t t1 = t0 + kZigTile < P ? t0 + kZigTile : P;
-    int emit = (int)(t1 - t0);
-    // positions of this tile swallowed by the previous tile's last attempt
-    for (int64_t p = t0; p < covered && p < t1; ++p) {
-      cs[p] |= 0x4000;
-      --emit;
-    }
     const int nsp = tile_nspec[(int64_t)s * ntiles + t];
-    const uint16_t* ts = tile_spec + ((int64_t)s * ntiles + t) * kZigTile;
-    for (int i = 0; i < nsp; ++i) {
-      const int64_t p = t0 + ts[i];
-      if (p < covered) continue;  // swallowed: not an attempt start (already counted)
-      const uint16_t c = cs[p];
-      const int consumed = c & 0x3fff;
-      if (!(c & 0x8000)) --emit;  // rejected attempt emits nothing
-      for (int64_t q = p + 1; q < p + consumed && q < t1; ++q) {
-        cs[q] |= 0x4000;
-        --emit;
+    const uint32_t* ts = tile_spec + ((int64_t)s * ntiles + t) * kZigTile;
+    for (int i = lane; i < nsp; i += 32) rec[i] = ts[i];
+    __syncwarp();
+    if (lane == 0) {
+      int niv = 0, removed = 0;
+      auto add = [&](int64_t a, int64_t b) {  // clip to this tile
+        if (a < t0) a = t0;
+        if (b > t1) b = t1;
+        if (b <= a) return;
+        const uint32_t ia = (uint32_t)(a - t0), ib = (uint32_t)(b - t0);
+        if (niv < kZigMaxIv) {
+          iv[niv++] = (ia << 16) | ib;
+        } else {
+          overflow = true;
+        }
+        removed += (int)(ib - ia);
+      };
+      if (covered > t0) add(t0, covered);  // swallowed by the previous tile's attempt
+      for (int i = 0; i < nsp; ++i) {
+        const uint32_t r = rec[i];
+        const int64_t p = t0 + (r & 1023u);
+        if (p < covered) continue;  // swallowed: not an attempt start
+        const int consumed = (int)((r >> 10) & 0x3fffu);
+        const bool acc = (r >> 31) & 1u;
+        add(acc ? p + 1 : p, p + consumed);
+        covered = p + consumed;
       }
-      covered = p + consumed;
+      if (covered < t1) covered = t1;
+      tile_niv[(int64_t)s * ntiles + t] = niv;
+      uint32_t* out = tile_iv + ((int64_t)s * ntiles + t) * kZigMaxIv;
+      for (int i = 0; i < niv; ++i) out[i] = iv[i];
+      const int emit = (int)(t1 - t0) - removed;
+      tile_emit[(int64_t)s * ntiles + t] = emit;
+      total += emit;
     }
-    if (covered < t1) covered = t1;
-    te[t] = emit;
-    total += emit;
+    __syncwarp();
   }
-  if (total < nvals) atomicOr(status, RGSV_ST_OMEGA_SHORT);  // margin exhausted
+  if (lane == 0 && (total < nvals || overflow)) atomicOr(status, RGSV_ST_OMEGA_SHORT);
 }
 
 // Per tile: exclusive prefix of emit flags -> output element index e; value
 // goes to Omega^T[e % k][e / k] (ld ldo) of stream s.
 __global__ void __launch_bounds__(kZigThreads) k_zig_scatter(
-    int64_t P, const double* __restrict__ val, const uint16_t* __restrict__ code,
-    const int* __restrict__ tile_emit, int64_t nvals, int k, double* __restrict__ out,
-    int64_t ldo, int64_t out_stride) {
+    int64_t P, const double* __restrict__ val, const int* __restrict__ tile_emit,
+    const int* __restrict__ tile_niv, const uint32_t* __restrict__ tile_iv, int64_t nvals, int k,
+    double* __restrict__ out, int64_t ldo, int64_t out_stride) {
   const int s = blockIdx.y;
   const int tile = blockIdx.x;
   const int ntiles = gridDim.x;
@@ -324,15 +353,23 @@ __global__ void __launch_bounds__(kZigThreads) k_zig_scatter(
     for (int t = 0; t < tile; ++t) b += te[t];
     tbase = b;
   }
+  __shared__ uint32_t iv[kZigMaxIv];
+  __shared__ int niv;
+  if (threadIdx.x == 0) niv = tile_niv[(int64_t)s * ntiles + tile];
+  __syncthreads();
+  for (int i = threadIdx.x; i < niv; i += blockDim.x)
+    iv[i] = tile_iv[((int64_t)s * ntiles + tile) * kZigMaxIv + i];
+  __syncthreads();
   const int64_t p0 = (int64_t)tile * kZigTile + threadIdx.x * kZigPerThread;
-  const uint16_t* cs = code + (int64_t)s * P;
   const double* vs = val + (int64_t)s * P;
   uint32_t emask = 0;
   for (int q = 0; q < kZigPerThread; ++q) {
     const int64_t p = p0 + q;
     if (p < P) {
-      const uint16_t c = cs[p];
-      if (!(c & 0x4000) && (c & 0x8000)) emask |= 1u << q;
+      const uint32_t off = (uint32_t)(threadIdx.x * kZigPerThread + q);
+      bool keep = true;
+      for (int i = 0; i < niv; ++i) keep &= !(off >= (iv[i] >> 16) && off < (iv[i] & 0xffffu));
+      if (keep) emask |= 1u << q;
     }
   }
   const int cnt = __popc(emask);
@@ -364,8 +401,9 @@ size_t omega_workspace_bytes(int nstreams, int64_t nvals) {
   b += (size_t)nstreams * sizeof(ZigStream) + 256;
   b += (size_t)nstreams * P * sizeof(double) + 256;
   b += (size_t)nstreams * P * sizeof(uint16_t) + 256;
-  b += (size_t)nstreams * ntiles * sizeof(int) * 2 + 512;
-  b += (size_t)nstreams * ntiles * kZigTile * sizeof(uint16_t) + 256;
+  b += (size_t)nstreams * ntiles * sizeof(int) * 3 + 768;
+  b += (size_t)nstreams * ntiles * kZigTile * sizeof(uint32_t) + 256;
+  b += (size_t)nstreams * ntiles * kZigMaxIv * sizeof(uint32_t) + 256;
   return b;
 }
 
@@ -389,17 +427,21 @@ int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double
   uint16_t* code = reinterpret_cast<uint16_t*>(take((size_t)nstreams * P * sizeof(uint16_t)));
   int* tnspec = reinterpret_cast<int*>(take((size_t)nstreams * ntiles * sizeof(int)));
   int* temit = reinterpret_cast<int*>(take((size_t)nstreams * ntiles * sizeof(int)));
-  uint16_t* tspec =
-      reinterpret_cast<uint16_t*>(take((size_t)nstreams * ntiles * kZigTile * sizeof(uint16_t)));
+  int* tniv = reinterpret_cast<int*>(take((size_t)nstreams * ntiles * sizeof(int)));
+  uint32_t* tspec =
+      reinterpret_cast<uint32_t*>(take((size_t)nstreams * ntiles * kZigTile * sizeof(uint32_t)));
+  uint32_t* tiv =
+      reinterpret_cast<uint32_t*>(take((size_t)nstreams * ntiles * kZigMaxIv * sizeof(uint32_t)));
   k_zig_seed<<<(nstreams + 127) / 128, 128, 0, st>>>(seeds, nstreams, streams);
   note_launch();
   dim3 grid(ntiles, nstreams);
   k_zig_attempt<<<grid, kZigThreads, 0, st>>>(streams, P, val, code, tnspec, tspec);
   note_launch();
-  k_zig_walk<<<(nstreams + 63) / 64, 64, 0, st>>>(nstreams, ntiles, P, nvals, code, tnspec, tspec,
-                                                  temit, status);
+  k_zig_walk<<<nstreams, 32, 0, st>>>(nstreams, ntiles, P, nvals, tnspec, tspec, temit, tniv,
+                                      tiv, status);
   note_launch();
-  k_zig_scatter<<<grid, kZigThreads, 0, st>>>(P, val, code, temit, nvals, k, out, ldo, out_stride);
+  k_zig_scatter<<<grid, kZigThreads, 0, st>>>(P, val, temit, tniv, tiv, nvals, k, out, ldo,
+                                              out_stride);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
