@@ -70,6 +70,25 @@ int rgsv_omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, d
                         int64_t ldo, int64_t out_stride, int* status, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* Omega block drawn from the running stream after skipping `offset` normals
+ * (the adaptive range finder draws block i right after blocks 0..i-1 from ONE
+ * generator, rangefinder.py:101,112). */
+size_t rgsv_omega_workspace_bytes_at(int nstreams, int64_t n, int k, int64_t offset);
+int rgsv_omega_generate_at(const uint64_t* seeds, int nstreams, int64_t n, int k, int64_t offset,
+                           double* out, int64_t ldo, int64_t out_stride, int* status,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Robust reduced QR of a tall block a (m x w, in place) by Householder in one
+ * CTA: q (m x min(m,w)), rdiag = |diag R| with the core.py:88-95 phase fix
+ * (diag R >= 0), tau (min(m,w)) scratch. Rank deficiency is allowed (R_jj = 0),
+ * like LAPACK dgeqr2 -- the adaptive range finder's trim test
+ * (rangefinder.py:120-121) reads rdiag. */
+int rgsv_householder_qr(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
+                        double* rdiag, double* tau, void* stream);
+/* y (rows x cols) += alpha * x (re-projection of rangefinder.py:116-118). */
+int rgsv_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
+              double alpha, void* stream);
+
 /* --- (1)-(3) range finder + projection for ONE matrix -------------------
  * Replaces rangefinder.extract_basis in fixed-rank mode (one block of
  * width k: rangefinder.py:106-133 with blocksize = max_cols = k,

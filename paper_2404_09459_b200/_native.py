@@ -43,6 +43,11 @@ SIGNATURES = {
     "rgsv_launch_count": (ctypes.c_longlong, []),
     "rgsv_omega_workspace_bytes": (_sz, [_i32, _i64, _i32]),
     "rgsv_omega_generate": (_i32, [_p, _i32, _i64, _i32, _p, _i64, _i64, _p, _p, _sz, _p]),
+    "rgsv_omega_workspace_bytes_at": (_sz, [_i32, _i64, _i32, _i64]),
+    "rgsv_omega_generate_at": (_i32, [_p, _i32, _i64, _i32, _i64, _p, _i64, _i64, _p, _p, _sz,
+                                      _p]),
+    "rgsv_householder_qr": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _p]),
+    "rgsv_axpy": (_i32, [_p, _i64, _p, _i64, _i32, _i32, _d, _p]),
     "rgsv_sketch_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "rgsv_sketch_project": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _i32, _i32, _p, _p, _i64, _p,
                                    _p, _p, _p, _sz, _p]),

@@ -24,6 +24,10 @@ int launch_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, doubl
                  double* part, int max_parts, cudaStream_t st);
 int launch_sum(const double* part, int n, double* out, cudaStream_t st);
 size_t householder_small_smem(int l);
+int launch_householder_tall(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
+                            double* rdiag, double* tau, cudaStream_t st);
+int launch_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
+                double alpha, cudaStream_t st);
 int debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
                               int64_t ld2, int l2, double* q, int64_t ldq, long long* prof,
                               cudaStream_t st);
@@ -147,6 +151,29 @@ int rgsv_omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, d
   if (nstreams < 1 || n < 1 || k < 1 || ldo < n) return RGSV_ERR_DIMENSION;
   return rgsv::omega_generate(seeds, nstreams, n, k, out, ldo, out_stride, status, workspace,
                               workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t rgsv_omega_workspace_bytes_at(int nstreams, int64_t n, int k, int64_t offset) {
+  return rgsv::omega_workspace_bytes(nstreams, n * (int64_t)k + offset);
+}
+
+int rgsv_omega_generate_at(const uint64_t* seeds, int nstreams, int64_t n, int k, int64_t offset,
+                           double* out, int64_t ldo, int64_t out_stride, int* status,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (nstreams < 1 || n < 1 || k < 1 || ldo < n || offset < 0) return RGSV_ERR_DIMENSION;
+  return rgsv::omega_generate(seeds, nstreams, n, k, out, ldo, out_stride, status, workspace,
+                              workspace_bytes, reinterpret_cast<cudaStream_t>(stream), offset);
+}
+
+int rgsv_householder_qr(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
+                        double* rdiag, double* tau, void* stream) {
+  return launch_householder_tall(a, lda, m, w, q, ldq, rdiag, tau,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
+              double alpha, void* stream) {
+  return launch_axpy(y, ldy, x, ldx, rows, cols, alpha, reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t rgsv_sketch_workspace_bytes(int64_t m, int64_t n, int k) {
@@ -290,8 +317,9 @@ SmallLayout small_layout(int l1, int l2, int64_t n) {
   L.linv = take((size_t)kmax * kmax * 8 + (size_t)kmax * (kmax + 1) * 8);
   L.rinv = take((size_t)kmax * kmax * 8);
   L.rdiag = take((size_t)kmax * 8);
-  L.v1 = take((size_t)(l1 + 1) * (kmax + 1) * 8 + (size_t)l1 * l * 8);
-  L.v2 = take((size_t)(l2 + 1) * (kmax + 1) * 8 + (size_t)l2 * l * 8);
+  const int64_t rmax = l < L.kpn ? l : L.kpn;  // columns of the stacked Q
+  L.v1 = take((size_t)(l1 + 1) * (rmax + 1) * 8);
+  L.v2 = take((size_t)(l2 + 1) * (rmax + 1) * 8);
   L.scratch_bytes = split_scratch_bytes(l, n, kmax) + (size_t)kSMs * kmax * kmax * 8;
   L.scratch = take(L.scratch_bytes);
   L.total = off;

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(32) k_zig_walk(int nstreams, int ntiles, int64
 __global__ void __launch_bounds__(kZigThreads) k_zig_scatter(
     int64_t P, const double* __restrict__ val, const int* __restrict__ tile_emit,
     const int* __restrict__ tile_niv, const uint32_t* __restrict__ tile_iv, int64_t nvals, int k,
-    double* __restrict__ out, int64_t ldo, int64_t out_stride) {
+    double* __restrict__ out, int64_t ldo, int64_t out_stride, int64_t offset) {
   const int s = blockIdx.y;
   const int tile = blockIdx.x;
   const int ntiles = gridDim.x;
@@ -388,13 +388,15 @@ __global__ void __launch_bounds__(kZigThreads) k_zig_scatter(
   double* o = out + (int64_t)s * out_stride;
   for (int q = 0; q < kZigPerThread; ++q) {
     if (emask & (1u << q)) {
-      if (e < nvals) o[(e % k) * ldo + e / k] = vs[p0 + q];
+      const int64_t f = e - offset;  // index within the requested block
+      if (f >= 0 && f < nvals) o[(f % k) * ldo + f / k] = vs[p0 + q];
       ++e;
     }
   }
 }
 
 size_t omega_workspace_bytes(int nstreams, int64_t nvals) {
+  // nvals counts every normal drawn, including a skipped prefix (offset)
   const int64_t P = nvals + nvals / 16 + 2 * kZigTile;
   const int64_t ntiles = (P + kZigTile - 1) / kZigTile;
   size_t b = 0;
@@ -411,11 +413,12 @@ size_t omega_workspace_bytes(int nstreams, int64_t nvals) {
 // out_stride between streams) from seeds[] (device array) on stream st.
 int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double* out,
                    int64_t ldo, int64_t out_stride, int* status, void* ws, size_t ws_bytes,
-                   cudaStream_t st) {
+                   cudaStream_t st, int64_t offset) {
   const int64_t nvals = n * (int64_t)k;
-  const int64_t P = nvals + nvals / 16 + 2 * kZigTile;
+  const int64_t nall = offset + nvals;  // the stream prefix is walked, then skipped
+  const int64_t P = nall + nall / 16 + 2 * kZigTile;
   const int ntiles = (int)((P + kZigTile - 1) / kZigTile);
-  if (ws_bytes < omega_workspace_bytes(nstreams, nvals)) return RGSV_ERR_WORKSPACE;
+  if (ws_bytes < omega_workspace_bytes(nstreams, nall)) return RGSV_ERR_WORKSPACE;
   char* p = static_cast<char*>(ws);
   auto take = [&](size_t bytes) {
     char* r = p;
@@ -437,11 +440,11 @@ int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double
   dim3 grid(ntiles, nstreams);
   k_zig_attempt<<<grid, kZigThreads, 0, st>>>(streams, P, val, code, tnspec, tspec);
   note_launch();
-  k_zig_walk<<<nstreams, 32, 0, st>>>(nstreams, ntiles, P, nvals, tnspec, tspec, temit, tniv,
+  k_zig_walk<<<nstreams, 32, 0, st>>>(nstreams, ntiles, P, nall, tnspec, tspec, temit, tniv,
                                       tiv, status);
   note_launch();
   k_zig_scatter<<<grid, kZigThreads, 0, st>>>(P, val, temit, tniv, tiv, nvals, k, out, ldo,
-                                              out_stride);
+                                              out_stride, offset);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }

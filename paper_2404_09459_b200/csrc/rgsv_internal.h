@@ -41,7 +41,7 @@ int chol_profile(const double* gram, int k, int kp, double* linv, long long* pro
 size_t omega_workspace_bytes(int nstreams, int64_t nvals);
 int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double* out,
                    int64_t ldo, int64_t out_stride, int* status, void* ws, size_t ws_bytes,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t offset = 0);
 
 struct Workspace {
   char* base;

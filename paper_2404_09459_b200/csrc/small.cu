@@ -471,6 +471,128 @@ int launch_householder_small(const double* b1, int64_t ld1, int l1, const double
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
+// --------------------------------------------- tall Householder QR (robust)
+// Q (m x w) and diag(R) of y (m x w) by Householder reflections in ONE CTA
+// over global (L2-resident) memory, with the phase fix of core.reduced_qr
+// (core.py:88-95: diag(R) >= 0). Rank-deficient input is fine: a zero column
+// gets tau = 0 and R_jj = 0, exactly like LAPACK dgeqr2. Used for the
+// adaptive range finder's blocks and as the CholeskyQR fallback; the matrix
+// is updated in place in `a` (m x w, ld lda), Q written to q.
+__global__ void __launch_bounds__(512) k_householder_tall(double* __restrict__ a, int64_t lda,
+                                                          int m, int w, double* __restrict__ q,
+                                                          int64_t ldq, double* __restrict__ rdiag,
+                                                          double* __restrict__ tau) {
+  __shared__ double wv[1024];
+  __shared__ double s_beta, s_scale, s_tau;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarp = nt >> 5;
+  const int kmin = m < w ? m : w;
+  for (int j = 0; j < kmin; ++j) {
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) ss = fma(a[i * lda + j], a[i * lda + j], ss);
+      ss = warp_sum(ss);
+      if (lane == 0) {
+        const double alpha = a[(int64_t)j * lda + j];
+        if (ss == 0.0) {
+          s_tau = 0.0;
+          s_scale = 0.0;
+          s_beta = alpha;
+        } else {
+          const double nrm = sqrt(fma(alpha, alpha, ss));
+          const double beta = alpha >= 0.0 ? -nrm : nrm;
+          s_tau = (beta - alpha) / beta;
+          s_scale = 1.0 / (alpha - beta);
+          s_beta = beta;
+        }
+        tau[j] = s_tau;
+      }
+    }
+    __syncthreads();
+    const double tj = s_tau, sc = s_scale;
+    for (int i = j + 1 + tid; i < m; i += nt) a[(int64_t)i * lda + j] *= sc;
+    if (tid == 0) a[(int64_t)j * lda + j] = s_beta;
+    __syncthreads();
+    if (tj != 0.0) {
+      for (int c = j + 1 + warp; c < w; c += nwarp) {
+        double acc = (lane == 0) ? a[(int64_t)j * lda + c] : 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32)
+          acc = fma(a[(int64_t)i * lda + j], a[(int64_t)i * lda + c], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) wv[c] = acc * tj;
+      }
+      __syncthreads();
+      for (int i = j + warp; i < m; i += nwarp) {
+        const double vi = (i == j) ? 1.0 : a[(int64_t)i * lda + j];
+        for (int c = j + 1 + lane; c < w; c += 32)
+          a[(int64_t)i * lda + c] = fma(-vi, wv[c], a[(int64_t)i * lda + c]);
+      }
+      __syncthreads();
+    }
+  }
+  // diag(R) and the phase fix: column j of Q is negated when R_jj < 0
+  __shared__ double sgn[1024];
+  for (int j = tid; j < kmin; j += nt) {
+    const double d = a[(int64_t)j * lda + j];
+    sgn[j] = d < 0.0 ? -1.0 : 1.0;
+    rdiag[j] = fabs(d);
+  }
+  // Q = H0 ... H_{k-1} [I; 0] (m x kmin), backwards in q
+  for (int i = warp; i < m; i += nwarp)
+    for (int c = lane; c < kmin; c += 32) q[(int64_t)i * ldq + c] = (i == c) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int j = kmin - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    for (int c = j + warp; c < kmin; c += nwarp) {
+      double acc = (lane == 0) ? q[(int64_t)j * ldq + c] : 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32)
+        acc = fma(a[(int64_t)i * lda + j], q[(int64_t)i * ldq + c], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) wv[c] = acc * tj;
+    }
+    __syncthreads();
+    for (int i = j + warp; i < m; i += nwarp) {
+      const double vi = (i == j) ? 1.0 : a[(int64_t)i * lda + j];
+      for (int c = j + lane; c < kmin; c += 32)
+        q[(int64_t)i * ldq + c] = fma(-vi, wv[c], q[(int64_t)i * ldq + c]);
+    }
+    __syncthreads();
+  }
+  for (int i = warp; i < m; i += nwarp)
+    for (int c = lane; c < kmin; c += 32) q[(int64_t)i * ldq + c] *= sgn[c];
+}
+
+int launch_householder_tall(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
+                            double* rdiag, double* tau, cudaStream_t st) {
+  if (w > 1024 || m < 1 || w < 1) return RGSV_ERR_DIMENSION;
+  k_householder_tall<<<1, 512, 0, st>>>(a, lda, m, w, q, ldq, rdiag, tau);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+// y (rows x cols) += alpha * x, strided
+__global__ void k_axpy(double* __restrict__ y, int64_t ldy, const double* __restrict__ x,
+                       int64_t ldx, int rows, int cols, double alpha) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    y[r * ldy + c] = fma(alpha, x[r * ldx + c], y[r * ldy + c]);
+  }
+}
+
+int launch_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
+                double alpha, cudaStream_t st) {
+  const int64_t total = (int64_t)rows * cols;
+  if (total <= 0) return 0;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 8 * kSMs) blocks = 8 * kSMs;
+  k_axpy<<<blocks, 256, 0, st>>>(y, ldy, x, ldx, rows, cols, alpha);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
 // ---------------------------------------------------------- comparative
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);

@@ -132,6 +132,64 @@ def omega_device(n: int, k: int, seeds, ldo: int | None = None) -> torch.Tensor:
     return out
 
 
+def omega_block(n: int, width: int, seed: int, offset: int, ldo: int) -> torch.Tensor:
+    """Omega^T (ceil16(width) x ldo) of block i of the adaptive range finder:
+    the n x width normals drawn from default_rng(seed) after `offset` earlier
+    normals (rangefinder.py:101,112), generated on the device."""
+    kp = ceil16(width)
+    out = torch.zeros((kp, ldo), dtype=F64, device="cuda")
+    sd = torch.tensor([seed_word(seed)], dtype=torch.int64).cuda()
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nb = int(lib().rgsv_omega_workspace_bytes_at(1, n, width, offset))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    check(lib().rgsv_omega_generate_at(vp(sd), 1, n, width, offset, vp(out), ldo, kp * ldo,
+                                       vp(status), vp(ws), nb, sp(torch.cuda.current_stream())),
+          "rgsv_omega_generate_at")
+    if int(status.item()) & _native.ST_OMEGA_SHORT:
+        raise RuntimeError("Omega generator exhausted its draw margin")
+    return out
+
+
+def small_spectrum(b1: torch.Tensor, l1: int, b2: torch.Tensor, l2: int, n: int,
+                   classify_tol: float) -> dict:
+    """Stacked QR + L-block singular values + fused comparative kernel for
+    arbitrary compressed blocks b1 (l1 x n), b2 (l2 x n) in HBM (row-major,
+    even pitch) -- engine.py:257-261 + :189-225 + analysis.py:82-102.
+    Returns host arrays (one D2H copy)."""
+    L = lib()
+    st = sp(torch.cuda.current_stream())
+    nb = int(L.rgsv_small_gsvd_workspace_bytes(l1, l2, n))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    res = torch.zeros(6 * n + 4 + 2 * max(l1, l2, 1) + 4, dtype=F64, device="cuda")
+    sv1 = res[6 * n + 4: 6 * n + 4 + max(l1, l2, 1)]
+    sv2 = res[6 * n + 4 + max(l1, l2, 1): 6 * n + 4 + 2 * max(l1, l2, 1)]
+    ints = torch.zeros(8, dtype=torch.int32, device="cuda")
+    status = ints[4:5]
+    dummy = torch.zeros(2, dtype=F64, device="cuda")
+    pb1 = vp(b1) if l1 else vp(dummy)
+    pb2 = vp(b2) if l2 else vp(dummy)
+    ld1 = b1.stride(0) if l1 else 2
+    ld2 = b2.stride(0) if l2 else 2
+    check(L.rgsv_small_gsvd(pb1, ld1, l1, pb2, ld2, l2, n, vp(sv1), vp(sv2), vp(ints[0:2]),
+                            vp(status), vp(ws), nb, st), "rgsv_small_gsvd")
+    check(L.rgsv_comparative(vp(sv1), vp(ints[0:2]), vp(sv2), n, float(classify_tol),
+                             *(vp(res[i * n:(i + 1) * n]) for i in range(6)),
+                             vp(res[6 * n: 6 * n + 4]), vp(ints[2:4]), vp(status), st),
+          "rgsv_comparative")
+    h = res.cpu().numpy()
+    iv = ints.cpu().numpy()
+    names = ("alphas", "betas", "rho", "theta", "p1", "p2")
+    out = {k: h[i * n:(i + 1) * n].copy() for i, k in enumerate(names)}
+    out["scalars"] = h[6 * n: 6 * n + 4].copy()
+    off = 6 * n + 4
+    w = max(l1, l2, 1)
+    out["sv1"] = h[off: off + int(iv[0])].copy()
+    out["sv2"] = h[off + w: off + w + int(iv[1])].copy()
+    out["counts"] = (int(iv[2]), int(iv[3]))
+    out["status"] = int(iv[4])
+    return out
+
+
 # ----------------------------------------------------------------- results
 class _Packed:
     """One device buffer + one pinned host mirror holding every small output

@@ -24,7 +24,13 @@ from .errors import (
     RecoveryError,
     ValidationError,
 )
-from .rangefinder import BasisResult, ExtractionConfig, check_max_cols, single_block_width
+from .rangefinder import (
+    BasisResult,
+    ExtractionConfig,
+    adaptive_device,
+    check_max_cols,
+    single_block_width,
+)
 
 RANDOMIZED = "randomized"
 DIRECT = "direct"
@@ -214,26 +220,64 @@ class DeviceRun:
     plan: object
 
 
-def _fixed_width(opts: GsvOptions, m: int, p: int, n: int) -> tuple[int, int]:
+def _fixed_width(opts: GsvOptions, m: int, p: int, n: int):
+    """(k1, k2) when both chains are one fixed-width block (the fused,
+    graph-captured pair pipeline), else None (direct or adaptive mode)."""
+    if opts.method == DIRECT:  # no extraction at all (engine.py:246-249)
+        return None
     cfg = opts.extraction
     check_max_cols(cfg, m, n)
     check_max_cols(cfg, p, n)
     w1 = single_block_width(cfg, m, n)
     w2 = single_block_width(cfg, p, n)
     if w1 is None or w2 is None:
-        raise ValidationError(
-            "the B200 pipeline runs the fixed-rank range finder: use "
-            "ExtractionConfig.fixed_rank(k, seed, power_iters) (max_cols <= blocksize, "
-            "trim_tol = 0); adaptive multi-block extraction is not implemented on the device yet")
-    if opts.method == DIRECT:
-        raise ValidationError("method='direct' is not implemented on the B200 path yet")
+        return None
     return w1, w2
+
+
+def _general_run(pair: GmpPair, opts: GsvOptions) -> DeviceRun:
+    """method='direct' and the adaptive range finder (engine.py:245-261):
+    compressed blocks C1, C2 built on the device (G itself for direct; Q^T G
+    from ``adaptive_device`` otherwise), then the shared stacked-QR +
+    L-block SVD + comparative stage (device.small_spectrum)."""
+    n = pair.n
+    if opts.method == DIRECT:
+        c1, c2 = pair.g1.t, pair.g2.t
+        l1, l2 = pair.m, pair.p
+        bases = (None, None)
+    else:
+        cfg = opts.extraction
+        q1, c1, b1 = adaptive_device(pair.g1, cfg)
+        q2, c2, b2 = adaptive_device(pair.g2, dataclasses.replace(cfg, seed=cfg.seed + 1))
+        b1.q, b2.q = q1, q2
+        l1, l2 = c1.shape[0], c2.shape[0]
+        bases = (b1, b2)
+    if l1 + l2 == 0:
+        raise RankDeficiencyError("both compressed blocks are empty")  # engine.py:258-259
+    out = _dev.small_spectrum(c1, l1, c2, l2, n, opts.classify_tol)
+    status = out["status"]
+    if status & ST_CHOL:
+        raise RankDeficiencyError("CholeskyQR breakdown: the stacked pair is numerically "
+                                  "rank deficient")
+    if status & ST_JACOBI:
+        raise ConvergenceError("Jacobi SVD of an L block did not converge")
+    if status & ST_CLASSIFY:
+        raise ValidationError("overlapping zero classifications; sequences not ordered?")
+    r, s = out["counts"]
+    spec = GsvSpectrum(out["alphas"], out["betas"], r, s)
+    sc = out["scalars"]
+    return DeviceRun(spec, spec.alphas, spec.betas, r, s, out["rho"], out["theta"], out["p1"],
+                     out["p2"], float(sc[0]), float(sc[1]), (float(sc[2]), float(sc[3])), status,
+                     bases[0], bases[1], out["sv1"], out["sv2"], None)
 
 
 def run_device_pipeline(pair: GmpPair, opts: GsvOptions, *, sync: bool = True) -> DeviceRun:
     """The randomized path of _run_pipeline + spectrum_from_l_blocks +
     analysis, on the device (engine.py:245-275, analysis.py:82-102)."""
-    k1, k2 = _fixed_width(opts, pair.m, pair.p, pair.n)
+    widths = _fixed_width(opts, pair.m, pair.p, pair.n)
+    if widths is None:
+        return _general_run(pair, opts)
+    k1, k2 = widths
     plan = _dev.pair_plan(pair.m, pair.p, pair.n, k1, k2)
     cfg = opts.extraction
     pk = plan.run(pair.g1, pair.g2, cfg.seed, cfg.power_iters, opts.classify_tol, sync=sync)
@@ -282,11 +326,15 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
     for pr in pairs[1:]:
         if (pr.m, pr.p, pr.n) != (first.m, first.p, first.n):
             raise DimensionError("compute_gsv_batch needs pairs of one shape")
-    k1, k2 = _fixed_width(opts, first.m, first.p, first.n)
     cfg = opts.extraction
     seeds = [cfg.seed] * len(pairs) if seeds is None else list(seeds)
     if len(seeds) != len(pairs):
         raise DimensionError("one seed per pair")
+    widths = _fixed_width(opts, first.m, first.p, first.n)
+    if widths is None:  # direct / adaptive: sequential general runs
+        return [_general_run(pr, dataclasses.replace(
+            opts, extraction=dataclasses.replace(cfg, seed=sd))) for pr, sd in zip(pairs, seeds)]
+    k1, k2 = widths
     plan = _dev.batch_plan(len(pairs), first.m, first.p, first.n, k1, k2)
     pks = plan.run([(pr.g1, pr.g2) for pr in pairs], seeds, cfg.power_iters, opts.classify_tol)
     return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]

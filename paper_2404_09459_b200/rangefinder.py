@@ -5,19 +5,25 @@ and adds ``power_iters`` (q, default 0 = reference behaviour; the
 BASELINE configs use q >= 1). ``extract_basis`` runs on
 the B200: one fixed-width block (the BASELINE configs' mode) is a single
 ``rgsv_sketch_project`` call — sketch Y = GΩ, shifted CholeskyQR3,
-q power iterations, projection B = QᵀG and its captured energy.
+q power iterations, projection B = QᵀG and its captured energy. The
+reference's default adaptive mode (several blocks, re-projection against the
+growing basis, rank trimming, early stop) runs as a host-driven loop of the
+same device kernels (``adaptive_device``), one host sync per block.
 """
 
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
 from . import device as _dev
-from ._native import ST_NONFINITE, lib
+from ._native import ST_CHOL, ST_NONFINITE, check, lib
+
+RGSV_ERR_WORKSPACE = 6  # include/rgsv_b200.h
 from .errors import DimensionError, RankDeficiencyError, ValidationError
 
 
@@ -84,20 +90,217 @@ def check_max_cols(cfg: ExtractionConfig, m: int, n: int) -> None:
         raise ValidationError(f"max_cols={cfg.max_cols} exceeds min(rows, cols)={min(m, n)}")
 
 
+class _Ops:
+    """The device kernels the adaptive loop strings together (C-ABI calls on
+    the current stream; scratch and status owned here)."""
+
+    def __init__(self):
+        self.L = lib()
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.scratch = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+
+    def st(self):
+        return _dev.sp(torch.cuda.current_stream())
+
+    def _scr(self, need: int):
+        if self.scratch.numel() < need:
+            self.scratch = torch.empty(need, dtype=torch.uint8, device="cuda")
+
+    def _gemm(self, fn, name, *args):
+        # split-K partials need scratch that depends on the tile plan: grow
+        # on RGSV_ERR_WORKSPACE (checked before any launch) and retry
+        while True:
+            rc = fn(*args, _dev.vp(self.scratch), self.scratch.numel(), self.st())
+            if rc != RGSV_ERR_WORKSPACE:
+                return check(rc, name)
+            self._scr(self.scratch.numel() * 4)
+
+    def gx(self, a, lda, bt, ldb, out, ldc, M, N, K):
+        """out (M x N) = A (M x K) Bt^T."""
+        self._gemm(self.L.rgsv_gemm_gx, "gemm_gx", a, lda, bt, ldb, out, ldc, M, N, K)
+
+    def gtq(self, a, lda, b, ldb, out, ldc, M, N, K):
+        """out (M x N) = A^T B with A: K x M, B: K x N."""
+        self._gemm(self.L.rgsv_gemm_gtq, "gemm_gtq", a, lda, b, ldb, out, ldc, M, N, K)
+
+    def chol(self, gram, k, kp, shift_rows):
+        linv = torch.zeros(kp * kp + kp * (kp + 1), dtype=torch.float64, device="cuda")
+        rinv = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")
+        rdiag = torch.zeros(kp, dtype=torch.float64, device="cuda")
+        check(self.L.rgsv_chol_inv(_dev.vp(gram), k, kp, shift_rows, _dev.vp(linv),
+                                   _dev.vp(rinv), _dev.vp(rdiag), _dev.vp(self.status),
+                                   self.st()), "chol_inv")
+        return linv[: kp * kp].view(kp, kp), rinv
+
+    def cholqr3(self, y, m, k, kp):
+        """Shifted CholeskyQR3 of y (m x kp, columns >= k zero): Q (m x kp)."""
+        for step in range(3):
+            gram = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")
+            self.gtq(_dev.vp(y), kp, _dev.vp(y), kp, _dev.vp(gram), kp, kp, kp, m)
+            linv, _ = self.chol(gram, k, kp, m if step == 0 else 0)
+            q = torch.zeros((m, kp), dtype=torch.float64, device="cuda")
+            self.gx(_dev.vp(y), kp, _dev.vp(linv), kp, _dev.vp(q), kp, m, kp, kp)
+            y = q
+        return y
+
+    def wide_cholqr3(self, zt, n, ldn, k, kp):
+        """Q of qr(Z) for Z = zt^T (zt: kp x ldn): returns Qhat^T (kp x ldn)."""
+        src = zt
+        for step in range(3):
+            gram = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")
+            self.gx(_dev.vp(src), ldn, _dev.vp(src), ldn, _dev.vp(gram), kp, kp, kp, n)
+            _, rinv = self.chol(gram, k, kp, n if step == 0 else 0)
+            dst = torch.zeros((kp, ldn), dtype=torch.float64, device="cuda")
+            self.gtq(_dev.vp(rinv), kp, _dev.vp(src), ldn, _dev.vp(dst), ldn, kp, n, kp)
+            src = dst
+        return src
+
+    def householder(self, y, m, w, kp):
+        """Robust QR (rgsv_householder_qr): Q (m x kp, zero-padded), |diag R|."""
+        a = y.clone()
+        q = torch.zeros((m, kp), dtype=torch.float64, device="cuda")
+        rd = torch.zeros(kp, dtype=torch.float64, device="cuda")
+        tau = torch.zeros(kp, dtype=torch.float64, device="cuda")
+        check(self.L.rgsv_householder_qr(_dev.vp(a), kp, m, w, _dev.vp(q), kp, _dev.vp(rd),
+                                         _dev.vp(tau), self.st()), "householder_qr")
+        return q, rd[: min(m, w)]
+
+    def reproject(self, y, m, wp, q, lqp):
+        """y -= Q (Q^T y), twice (rangefinder.py:116-118)."""
+        for _ in range(2):
+            tt = torch.zeros((wp, lqp), dtype=torch.float64, device="cuda")
+            self.gtq(_dev.vp(y), wp, _dev.vp(q), q.stride(0), _dev.vp(tt), lqp, wp, lqp, m)
+            proj = torch.zeros((m, wp), dtype=torch.float64, device="cuda")
+            self.gx(_dev.vp(q), q.stride(0), _dev.vp(tt), lqp, _dev.vp(proj), wp, m, wp, lqp)
+            check(self.L.rgsv_axpy(_dev.vp(y), wp, _dev.vp(proj), wp, m, wp, -1.0, self.st()),
+                  "axpy")
+
+    def sumsq(self, a, lda, rows, cols) -> float:
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ws = torch.zeros(1024, dtype=torch.float64, device="cuda")
+        check(self.L.rgsv_sumsq(a, lda, rows, cols, _dev.vp(out), _dev.vp(ws), 8192,
+                                self.st()), "sumsq")
+        return float(out.item())
+
+
+def _block_qr(ops: _Ops, y, m: int, w: int, wp: int, trim_cut: float):
+    """reduced_qr of one sketch block with the reference's phase (core.py:80-95)
+    and |diag R| for the trim test. Well-conditioned blocks take shifted
+    CholeskyQR3 (R_jj = q_j^T y_j from one small GEMM); blocks whose R is
+    near the trim threshold or numerically rank deficient -- where the trim
+    decision needs Householder's rank-revealing diagonal -- take the robust
+    one-CTA Householder kernel."""
+    mode = os.environ.get("RGSV_ADAPTIVE_QR", "auto")  # diagnostics: auto|householder
+    if m >= w and mode != "householder":
+        ops.status.zero_()
+        q = ops.cholqr3(y, m, w, wp)
+        r = torch.zeros((wp, wp), dtype=torch.float64, device="cuda")
+        ops.gtq(_dev.vp(q), wp, _dev.vp(y), wp, _dev.vp(r), wp, wp, wp, m)
+        rd = torch.diagonal(r)[:w].abs().cpu().numpy()
+        ok = (int(ops.status.item()) & (ST_CHOL | ST_NONFINITE)) == 0
+        if ok and np.all(np.isfinite(rd)) and rd.min() >= max(1e3 * trim_cut,
+                                                               1e-8 * rd.max()):
+            return q, rd
+    q, rd = ops.householder(y, m, w, wp)
+    return q, rd.cpu().numpy()
+
+
+def adaptive_device(a: "_dev.DevMatrix", cfg: ExtractionConfig):
+    """Alg. 1 (rangefinder.py:68-135) on the device. Returns
+    (Q: m x lq tensor, B = Q^T G: lq x ldn tensor, BasisResult). Block i's
+    Omega continues the ONE generator stream (offset = normals drawn so far),
+    so every block is bit-identical to the reference's draw."""
+    ops = _Ops()
+    m, n = a.rows, a.cols
+    ldn = _dev.ceil16(n)
+    gf2 = _dev.device_sumsq(a)                                   # :83
+    if not math.isfinite(gf2):
+        raise ValidationError("g contains non-finite entries")
+    normf = math.sqrt(gf2)
+    tol = cfg.tol if cfg.tol is not None else 1e-10 * normf      # :85
+    trim_cut = cfg.trim_tol * normf                              # :86
+    # every sampled column may be kept (trim_tol = 0 keeps noise columns too,
+    # rangefinder.py:120-124), so the basis can hold up to n (or max_cols)
+    cap = n if cfg.max_cols is None else cfg.max_cols
+    capp = _dev.ceil16(cap)
+    qb = torch.zeros((m, capp), dtype=torch.float64, device="cuda")
+    bb = torch.zeros((capp, ldn), dtype=torch.float64, device="cuda")
+    history = [normf]
+    widths: list = []
+    lq = 0
+    if normf == 0.0 or normf < tol:                              # :96
+        return qb[:, :0], bb[:0], BasisResult(None, history, True, 0, widths)
+    b = min(cfg.blocksize, n)                                    # :99
+    nblocks = -(-n // b)
+    captured: list = []
+    converged = False
+    iterations = 0
+    offset = 0
+    for i in range(nblocks):                                     # :106
+        width = min(b, n - i * b)
+        if cfg.max_cols is not None:
+            width = min(width, cfg.max_cols - lq)
+            if width <= 0:
+                break
+        wp = _dev.ceil16(width)
+        om = _dev.omega_block(n, width, cfg.seed, offset, ldn)    # :112
+        offset += n * width
+        y = torch.zeros((m, wp), dtype=torch.float64, device="cuda")
+        ops.gx(_dev.vp(a.t), a.ld, _dev.vp(om), ldn, _dev.vp(y), wp, m, wp, n)  # :115
+        lqp = _dev.ceil16(lq)
+        if lq:
+            ops.reproject(y, m, wp, qb, lqp)                     # :116-118
+        for _ in range(cfg.power_iters):
+            p, _ = _block_qr(ops, y, m, width, wp, 0.0)
+            zt = torch.zeros((wp, ldn), dtype=torch.float64, device="cuda")
+            ops.gtq(_dev.vp(p), wp, _dev.vp(a.t), a.ld, _dev.vp(zt), ldn, wp, n, m)
+            qht = ops.wide_cholqr3(zt, n, ldn, width, wp)
+            y = torch.zeros((m, wp), dtype=torch.float64, device="cuda")
+            ops.gx(_dev.vp(a.t), a.ld, _dev.vp(qht), ldn, _dev.vp(y), wp, m, wp, n)
+            if lq:
+                ops.reproject(y, m, wp, qb, lqp)
+        p, rd = _block_qr(ops, y, m, width, wp, trim_cut)        # :119
+        keep = np.flatnonzero(rd >= trim_cut)                    # :120-121
+        kc = int(keep.size)
+        if kc:
+            pk = torch.zeros((m, wp), dtype=torch.float64, device="cuda")
+            if kc == width:
+                pk.copy_(p)
+            else:
+                pk[:, :kc] = p[:, torch.from_numpy(keep).cuda()]
+            blk = torch.zeros((wp, ldn), dtype=torch.float64, device="cuda")
+            ops.gtq(_dev.vp(pk), wp, _dev.vp(a.t), a.ld, _dev.vp(blk), ldn, wp, n, m)
+            captured.append(ops.sumsq(_dev.vp(blk), ldn, kc, n))  # :123
+            qb[:, lq: lq + kc] = pk[:, :kc]                      # :124
+            bb[lq: lq + kc] = blk[:kc]
+            lq += kc
+        widths.append(kc)
+        res2 = gf2 - math.fsum(captured)                         # :126
+        history.append(math.sqrt(max(res2, 0.0)))
+        iterations = i + 1
+        if history[-1] < tol:                                    # :129-131
+            converged = True
+            break
+        if cfg.max_cols is not None and lq >= cfg.max_cols:      # :132-133
+            break
+    return qb[:, :lq], bb[:lq], BasisResult(None, history, converged, iterations, widths)
+
+
 def extract_basis(g, cfg: ExtractionConfig | None = None, *, device_result: bool = False):
     """Extract an approximate orthonormal basis of range(g) on the B200
     (rangefinder.py:68-135). Returns the reference's ``BasisResult``; with
-    ``device_result=True`` the basis stays in HBM as a torch tensor."""
+    ``device_result=True`` the basis stays in HBM as a torch tensor. A
+    fixed-width single block takes the fused ``rgsv_sketch_project`` call;
+    any other configuration runs ``adaptive_device``."""
     cfg = cfg or ExtractionConfig()
     a = _dev.to_device(g, "g")
     m, n = a.rows, a.cols
     check_max_cols(cfg, m, n)
     width = single_block_width(cfg, m, n)
     if width is None:
-        raise ValidationError(
-            "the B200 range finder runs the single-block (fixed-rank) mode: set "
-            "max_cols <= blocksize (or blocksize >= n) and trim_tol = 0; adaptive multi-block "
-            "extraction is not implemented on the device yet")
+        q, _, res = adaptive_device(a, cfg)
+        res.q = q if device_result else q.cpu().numpy()
+        return res
     plan = _dev.SketchPlan(m, n, width)
     stats = torch.zeros(2, dtype=torch.float64, device="cuda")
     rdiag = torch.zeros(max(width, 1), dtype=torch.float64, device="cuda")
