@@ -85,6 +85,28 @@ int rgsv_omega_generate_at(const uint64_t* seeds, int nstreams, int64_t n, int k
  * (rangefinder.py:120-121) reads rdiag. */
 int rgsv_householder_qr(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
                         double* rdiag, double* tau, void* stream);
+/* --- recover_gsvd building blocks (engine.py:278-362) ------------------- */
+/* Orthonormal completion (engine.py:278-291): `count` orthonormal columns
+ * orthogonal to the `have` orthonormal columns of a (dim x have, overwritten
+ * by its Householder factorization) -- columns have..have+count of the
+ * complete Q, like numpy.linalg.qr(mode="complete"). out: dim x count. */
+int rgsv_orth_complete(double* a, int64_t lda, int dim, int have, int count, double* out,
+                       int64_t ldo, double* rdiag, double* tau, void* stream);
+/* One-sided Jacobi SVD with vectors of the nv rows of v (nv x len, in
+ * place): acc (nv x nv) scratch, sv[nv] sorted (descending, or ascending),
+ * xn (nv x len) unit singular rows, jo (nv x nv) the matching rotation rows;
+ * A (rows as vectors) = jo^T diag(sv) xn. *nzero = exactly-zero values
+ * (their xn rows are 0; the caller completes them). Replaces the full SVDs
+ * np.linalg.svd(L, full_matrices=True) of engine.py:322,340. */
+int rgsv_svd_vectors(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                     double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj, int ascending,
+                     int* nzero, int* status, void* stream);
+/* dst (cols x rows) = src^T, src rows x cols. */
+int rgsv_transpose(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
+                   void* stream);
+/* a[:, j] /= d[j] for j < cols (engine.py:335,357). */
+int rgsv_scale_cols(double* a, int64_t lda, int rows, int cols, const double* d, void* stream);
+
 /* y (rows x cols) += alpha * x (re-projection of rangefinder.py:116-118). */
 int rgsv_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
               double alpha, void* stream);

@@ -48,6 +48,11 @@ SIGNATURES = {
                                       _p]),
     "rgsv_householder_qr": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _p]),
     "rgsv_axpy": (_i32, [_p, _i64, _p, _i64, _i32, _i32, _d, _p]),
+    "rgsv_orth_complete": (_i32, [_p, _i64, _i32, _i32, _i32, _p, _i64, _p, _p, _p]),
+    "rgsv_svd_vectors": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _i64, _p, _i64, _i32,
+                                _p, _p, _p]),
+    "rgsv_transpose": (_i32, [_p, _i64, _p, _i64, _i32, _i32, _p]),
+    "rgsv_scale_cols": (_i32, [_p, _i64, _i32, _i32, _p, _p]),
     "rgsv_sketch_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "rgsv_sketch_project": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _i32, _i32, _p, _p, _i64, _p,
                                    _p, _p, _p, _sz, _p]),

@@ -25,7 +25,12 @@ int launch_sumsq(const double* a, int64_t lda, int64_t rows, int64_t cols, doubl
 int launch_sum(const double* part, int n, double* out, cudaStream_t st);
 size_t householder_small_smem(int l);
 int launch_householder_tall(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
-                            double* rdiag, double* tau, cudaStream_t st);
+                            double* rdiag, double* tau, int comp_count, cudaStream_t st);
+int launch_jacobi_vec(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                      double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj, int ascending,
+                      int* nzero, int* status, cudaStream_t st);
+int launch_scale_cols(double* a, int64_t lda, int rows, int cols, const double* d,
+                      cudaStream_t st);
 int launch_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
                 double alpha, cudaStream_t st);
 int debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
@@ -167,8 +172,33 @@ int rgsv_omega_generate_at(const uint64_t* seeds, int nstreams, int64_t n, int k
 
 int rgsv_householder_qr(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
                         double* rdiag, double* tau, void* stream) {
-  return launch_householder_tall(a, lda, m, w, q, ldq, rdiag, tau,
+  return launch_householder_tall(a, lda, m, w, q, ldq, rdiag, tau, 0,
                                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_orth_complete(double* a, int64_t lda, int dim, int have, int count, double* out,
+                       int64_t ldo, double* rdiag, double* tau, void* stream) {
+  if (count < 1 || have < 0 || have + count > dim) return RGSV_ERR_DIMENSION;
+  return launch_householder_tall(a, lda, dim, have, out, ldo, rdiag, tau, count,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_svd_vectors(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                     double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj, int ascending,
+                     int* nzero, int* status, void* stream) {
+  return launch_jacobi_vec(v, ldv, nv, len, acc, ldacc, sv, xn, ldx, jo, ldj, ascending, nzero,
+                           status, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_transpose(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
+                   void* stream) {
+  if (rows < 0 || cols < 0 || ldd < rows || lds < cols) return RGSV_ERR_DIMENSION;
+  return launch_copy_block(dst, ldd, src, lds, cols, rows, 1,
+                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_scale_cols(double* a, int64_t lda, int rows, int cols, const double* d, void* stream) {
+  return launch_scale_cols(a, lda, rows, cols, d, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rgsv_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,

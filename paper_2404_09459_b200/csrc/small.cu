@@ -138,6 +138,140 @@ __global__ void __launch_bounds__(1024) k_jacobi_rows(JacobiJob j0, JacobiJob j1
   if (tid == 0) *J.nsv_out = nout;
 }
 
+// ------------------------------------------- Jacobi SVD with vectors
+// One-sided Jacobi on the nv rows of v (nv x len, in place) with the
+// rotations accumulated into acc (nv x nv, starts at I): J v = diag(s) X with
+// orthogonal rows of X. Outputs, ordered by singular value (descending, or
+// ascending when `ascending`): sv[nv], xn (nv x len) = the unit rows of X
+// (a zero row stays zero and is counted in *nzero for the caller's
+// completion), jo (nv x nv) = the matching rows of J. For A with rows as
+// vectors, A = J^T diag(s) X: U = jo^T, V^H = xn. Serves recover_gsvd's
+// full SVDs of the L blocks (engine.py:322,340) -- off the hot path, so the
+// vectors stay in global (L2-resident) memory.
+__global__ void __launch_bounds__(512) k_jacobi_vec(double* __restrict__ v, int64_t ldv, int nv,
+                                                    int len, double* __restrict__ acc,
+                                                    int64_t ldacc, double* __restrict__ sv,
+                                                    double* __restrict__ xn, int64_t ldx,
+                                                    double* __restrict__ jo, int64_t ldj,
+                                                    int ascending, int max_sweeps,
+                                                    int* __restrict__ nzero,
+                                                    int* __restrict__ status) {
+  __shared__ double nrm[kJacobiMaxVec];
+  __shared__ int ord[kJacobiMaxVec];
+  __shared__ int s_zero;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  for (int i = warp; i < nv; i += nwarps)
+    for (int e = lane; e < nv; e += 32) acc[(int64_t)i * ldacc + e] = (i == e) ? 1.0 : 0.0;
+  if (tid == 0) s_zero = 0;
+  __syncthreads();
+  const int nve = nv + (nv & 1);
+  const double tol = fmax(1e-15, sqrt((double)len) * 2.220446049250313e-16);
+  bool converged = (nv == 1);
+  for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < nve - 1; ++round) {
+      for (int p = warp; p < nve / 2; p += nwarps) {
+        const int a = rr_index(p, round, nve), b = rr_index(nve - 1 - p, round, nve);
+        if (a >= nv || b >= nv) continue;
+        double* va = v + (int64_t)a * ldv;
+        double* vb = v + (int64_t)b * ldv;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int e = lane; e < len; e += 32) {
+          const double x = va[e], y = vb[e];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int e = lane; e < len; e += 32) {
+            const double x = va[e], y = vb[e];
+            va[e] = c * x - s * y;
+            vb[e] = s * x + c * y;
+          }
+          double* ja = acc + (int64_t)a * ldacc;
+          double* jb = acc + (int64_t)b * ldacc;
+          for (int e = lane; e < nv; e += 32) {
+            const double x = ja[e], y = jb[e];
+            ja[e] = c * x - s * y;
+            jb[e] = s * x + c * y;
+          }
+          rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    converged = !__syncthreads_or(rotated);
+  }
+  if (!converged && tid == 0) atomicOr(status, RGSV_ST_JACOBI);
+  for (int i = warp; i < nv; i += nwarps) {
+    const double* vi = v + (int64_t)i * ldv;
+    double s = 0.0;
+    for (int e = lane; e < len; e += 32) s = fma(vi[e], vi[e], s);
+    s = warp_sum(s);
+    if (lane == 0) nrm[i] = sqrt(s);
+  }
+  __syncthreads();
+  for (int i = tid; i < nv; i += blockDim.x) {
+    const double x = nrm[i];
+    int rank = 0;
+    for (int j = 0; j < nv; ++j) {
+      const double y = nrm[j];
+      rank += ascending ? ((y < x) || (y == x && j < i)) : ((y > x) || (y == x && j < i));
+    }
+    ord[rank] = i;
+    sv[rank] = x;
+    if (x == 0.0) atomicAdd(&s_zero, 1);
+  }
+  __syncthreads();
+  for (int r = warp; r < nv; r += nwarps) {
+    const int i = ord[r];
+    const double x = nrm[i];
+    const double inv = x > 0.0 ? 1.0 / x : 0.0;
+    for (int e = lane; e < len; e += 32) xn[(int64_t)r * ldx + e] = v[(int64_t)i * ldv + e] * inv;
+    for (int e = lane; e < nv; e += 32) jo[(int64_t)r * ldj + e] = acc[(int64_t)i * ldacc + e];
+  }
+  if (tid == 0) *nzero = s_zero;
+}
+
+int launch_jacobi_vec(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                      double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj, int ascending,
+                      int* nzero, int* status, cudaStream_t st) {
+  if (nv < 1 || len < 1 || nv > kJacobiMaxVec) return RGSV_ERR_DIMENSION;
+  k_jacobi_vec<<<1, 512, 0, st>>>(v, ldv, nv, len, acc, ldacc, sv, xn, ldx, jo, ldj, ascending,
+                                  60, nzero, status);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
+// a (rows x cols) column j scaled by 1/d[j] (recover_gsvd, engine.py:335,357)
+__global__ void k_scale_cols(double* __restrict__ a, int64_t lda, int rows, int cols,
+                             const double* __restrict__ d) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols;
+    const int c = (int)(e % cols);
+    a[r * lda + c] = a[r * lda + c] / d[c];
+  }
+}
+
+int launch_scale_cols(double* a, int64_t lda, int rows, int cols, const double* d,
+                      cudaStream_t st) {
+  const int64_t total = (int64_t)rows * cols;
+  if (total <= 0) return 0;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 8 * kSMs) blocks = 8 * kSMs;
+  k_scale_cols<<<blocks, 256, 0, st>>>(a, lda, rows, cols, d);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
 // ------------------------------------------------------ Householder QR
 // Q of the Householder QR of the l x l leading block T = S[:, :l] of the
 // stacked S = [B1; B2] (l <= n). LAPACK dgeqrf/dorgqr (numpy.linalg.qr,
@@ -481,7 +615,8 @@ int launch_householder_small(const double* b1, int64_t ld1, int l1, const double
 __global__ void __launch_bounds__(512) k_householder_tall(double* __restrict__ a, int64_t lda,
                                                           int m, int w, double* __restrict__ q,
                                                           int64_t ldq, double* __restrict__ rdiag,
-                                                          double* __restrict__ tau) {
+                                                          double* __restrict__ tau,
+                                                          int comp_count) {
   __shared__ double wv[1024];
   __shared__ double s_beta, s_scale, s_tau;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
@@ -530,6 +665,34 @@ __global__ void __launch_bounds__(512) k_householder_tall(double* __restrict__ a
       __syncthreads();
     }
   }
+  if (comp_count > 0) {
+    // orthonormal completion (engine.py:278-291): columns kmin .. kmin+count
+    // of the COMPLETE Q = H0 .. H_{k-1} (numpy.linalg.qr mode="complete"),
+    // i.e. the reflectors applied to e_kmin .. e_{kmin+count-1}; no phase fix
+    for (int i = warp; i < m; i += nwarp)
+      for (int c = lane; c < comp_count; c += 32)
+        q[(int64_t)i * ldq + c] = (i == kmin + c) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int j = kmin - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      for (int c = warp; c < comp_count; c += nwarp) {
+        double acc = (lane == 0) ? q[(int64_t)j * ldq + c] : 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32)
+          acc = fma(a[(int64_t)i * lda + j], q[(int64_t)i * ldq + c], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) wv[c] = acc * tj;
+      }
+      __syncthreads();
+      for (int i = j + warp; i < m; i += nwarp) {
+        const double vi = (i == j) ? 1.0 : a[(int64_t)i * lda + j];
+        for (int c = lane; c < comp_count; c += 32)
+          q[(int64_t)i * ldq + c] = fma(-vi, wv[c], q[(int64_t)i * ldq + c]);
+      }
+      __syncthreads();
+    }
+    return;
+  }
   // diag(R) and the phase fix: column j of Q is negated when R_jj < 0
   __shared__ double sgn[1024];
   for (int j = tid; j < kmin; j += nt) {
@@ -564,9 +727,11 @@ __global__ void __launch_bounds__(512) k_householder_tall(double* __restrict__ a
 }
 
 int launch_householder_tall(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
-                            double* rdiag, double* tau, cudaStream_t st) {
-  if (w > 1024 || m < 1 || w < 1) return RGSV_ERR_DIMENSION;
-  k_householder_tall<<<1, 512, 0, st>>>(a, lda, m, w, q, ldq, rdiag, tau);
+                            double* rdiag, double* tau, int comp_count, cudaStream_t st) {
+  if (w > 1024 || comp_count > 1024 || m < 1 || w < 0 || comp_count < 0) return RGSV_ERR_DIMENSION;
+  if (w == 0 && comp_count == 0) return RGSV_ERR_DIMENSION;
+  if (comp_count > 0 && (w > m || w + comp_count > m)) return RGSV_ERR_DIMENSION;
+  k_householder_tall<<<1, 512, 0, st>>>(a, lda, m, w, q, ldq, rdiag, tau, comp_count);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }

@@ -235,6 +235,28 @@ def _fixed_width(opts: GsvOptions, m: int, p: int, n: int):
     return w1, w2
 
 
+def _small_checked(c1, l1: int, c2, l2: int, n: int, classify_tol: float) -> dict:
+    """device.small_spectrum + the reference's error mapping."""
+    out = _dev.small_spectrum(c1, l1, c2, l2, n, classify_tol)
+    status = out["status"]
+    if status & ST_CHOL:
+        raise RankDeficiencyError("CholeskyQR breakdown: the stacked pair is numerically "
+                                  "rank deficient")
+    if status & ST_JACOBI:
+        raise ConvergenceError("Jacobi SVD of an L block did not converge")
+    if status & ST_CLASSIFY:
+        raise ValidationError("overlapping zero classifications; sequences not ordered?")
+    return out
+
+
+def _spectrum_checked(c1, l1: int, c2, l2: int, n: int, classify_tol: float) -> GsvSpectrum:
+    if l1 + l2 == 0:
+        raise RankDeficiencyError("both compressed blocks are empty")
+    out = _small_checked(c1, l1, c2, l2, n, classify_tol)
+    r, s = out["counts"]
+    return GsvSpectrum(out["alphas"], out["betas"], r, s)
+
+
 def _general_run(pair: GmpPair, opts: GsvOptions) -> DeviceRun:
     """method='direct' and the adaptive range finder (engine.py:245-261):
     compressed blocks C1, C2 built on the device (G itself for direct; Q^T G
@@ -254,15 +276,8 @@ def _general_run(pair: GmpPair, opts: GsvOptions) -> DeviceRun:
         bases = (b1, b2)
     if l1 + l2 == 0:
         raise RankDeficiencyError("both compressed blocks are empty")  # engine.py:258-259
-    out = _dev.small_spectrum(c1, l1, c2, l2, n, opts.classify_tol)
+    out = _small_checked(c1, l1, c2, l2, n, opts.classify_tol)
     status = out["status"]
-    if status & ST_CHOL:
-        raise RankDeficiencyError("CholeskyQR breakdown: the stacked pair is numerically "
-                                  "rank deficient")
-    if status & ST_JACOBI:
-        raise ConvergenceError("Jacobi SVD of an L block did not converge")
-    if status & ST_CLASSIFY:
-        raise ValidationError("overlapping zero classifications; sequences not ordered?")
     r, s = out["counts"]
     spec = GsvSpectrum(out["alphas"], out["betas"], r, s)
     sc = out["scalars"]
@@ -354,21 +369,19 @@ def compute_gsv(pair: GmpPair, opts: GsvOptions | None = None) -> GsvSpectrum:
 
 
 def recover_gsvd(pair: GmpPair, opts: GsvOptions | None = None) -> GsvdFactors:
-    """Full decomposition recovery (engine.py:294-362). Requires m, p >= n
-    (:304-307) and an R-tilde with n rows (:309-313); in the fixed-rank mode
-    with l1 + l2 < n (every BASELINE config) the reference
-    raises RecoveryError, and so does this path."""
+    """Full decomposition recovery (engine.py:294-362) on the device
+    (recovery.py). Requires m, p >= n (:304-307) and a compressed pair with
+    n independent columns (:309-313): the fixed-rank BASELINE configs have
+    l1 + l2 = 2k < n and raise RecoveryError exactly like
+    the reference; the adaptive default and method="direct" recover."""
+    from .recovery import recover
+
     opts = opts or GsvOptions()
-    m, p, n = pair.m, pair.p, pair.n
-    if m < n or p < n:
-        raise RecoveryError(f"full recovery needs m >= n and p >= n, got ({m}, {p}, {n})")
-    k1, k2 = _fixed_width(opts, m, p, n)
-    if min(k1 + k2, n) != n:
-        raise RecoveryError(
-            "compressed pair has fewer than n independent columns; "
-            "tighten the extraction tolerance")
-    raise RecoveryError("GSVD factor recovery with l1 + l2 >= n is not implemented on the "
-                        "B200 path yet")
+    if opts.method != DIRECT:
+        check_max_cols(opts.extraction, pair.m, pair.n)
+        check_max_cols(opts.extraction, pair.p, pair.n)
+    u, v, rf, spec = recover(pair, opts, opts.method == DIRECT)
+    return GsvdFactors(u, v, rf, spec)
 
 
 __all__ = ["GmpPair", "GsvSpectrum", "GsvOptions", "GsvdFactors", "classify_spectrum",
