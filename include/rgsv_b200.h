@@ -85,6 +85,34 @@ int rgsv_omega_generate_at(const uint64_t* seeds, int nstreams, int64_t n, int k
  * (rangefinder.py:120-121) reads rdiag. */
 int rgsv_householder_qr(double* a, int64_t lda, int m, int w, double* q, int64_t ldq,
                         double* rdiag, double* tau, void* stream);
+/* --- batched small pairs ----------------------------
+ * compute_gsv + compare for npairs independent same-k pairs in ~6 launches:
+ * Omega for every matrix (seeds[2j], seeds[2j+1] -- the reference draws G2's
+ * Omega from seed + 1, engine.py:252-253), one cluster-per-matrix fused
+ * chain kernel (sketch, shifted CholeskyQR3 in shared memory, q power
+ * iterations, projection B = Q^T G), then one CTA per pair for the stacked
+ * QR + Jacobi + comparative stage. mats: device array of 2*npairs
+ * descriptors {G1_0, G2_0, G1_1, ...}; n <= 128, k <= 32, 2k <= n.
+ * Per pair outputs: res[j*(6n+4+2k)] = {alphas, betas, rho, theta, p1, p2,
+ * scalars[4] (d1, d2, sum p1, sum p2), sv1[k], sv2[k]}; ints[4j] = {nsv1,
+ * nsv2, r, s}; stats[4j] = {|G1|^2, |B1|^2, |G2|^2, |B2|^2}; status[j].
+ * b_out (optional, else workspace): the projections B of every matrix,
+ * 2*npairs blocks of kp x ceil16(n) (kp = 16 or 32), rows >= k zero. */
+typedef struct {
+  const double* g;
+  int64_t ld;
+  int32_t rows;
+  int32_t pad;
+} rgsv_matrix_desc;
+/* 1 when rgsv_batch_gsvd serves this shape (the per-CTA Y slice of the
+ * largest matrix fits shared memory in a cluster of <= 8 CTAs), else 0. */
+int rgsv_batch_supported(int max_rows, int64_t n, int k);
+size_t rgsv_batch_workspace_bytes(int npairs, int64_t n, int k);
+int rgsv_batch_gsvd(const void* mats, int npairs, int max_rows, int64_t n, int k, int q,
+                    const uint64_t* seeds, double classify_tol, double* res, int* ints,
+                    double* stats, int* status, double* b_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* --- recover_gsvd building blocks (engine.py:278-362) ------------------- */
 /* Orthonormal completion (engine.py:278-291): `count` orthonormal columns
  * orthogonal to the `have` orthonormal columns of a (dim x have, overwritten

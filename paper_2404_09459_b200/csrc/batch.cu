@@ -1,0 +1,608 @@
+// Batched fixed-rank rGSVD chains for many small pairs (SURVEY.md §8 cfg3:
+// 4096 pairs of 4000/3000 x 64, k = 16, q = 1).
+//
+// One thread-block CLUSTER per matrix G (m x n): the cluster's CS CTAs split
+// G's rows, and each CTA keeps its slice of the sketch Y / basis Q in SHARED
+// MEMORY for the whole chain, so shifted CholeskyQR3 (Gram, Cholesky, TRSM)
+// never touches HBM. G is streamed through cp.async tiles (32 rows x n) into
+// FP64 DMMA (mma.sync.m8n8k4) four times per chain (sketch, G^T Q, G Q^,
+// projection); with only ~148/CS matrices in flight the re-reads come from
+// L2. The k x k Gram and n x k partial products are reduced across the
+// cluster through distributed shared memory (mapa + ld.shared::cluster) in a
+// fixed CTA order, so every CTA holds bit-identical small matrices and the
+// result does not depend on scheduling. Per matrix the chain is the same
+// algorithm as rgsv_sketch_project (rangefinder.py:115-123 + the q power
+// iterations of SURVEY.md §8(c)): Y = G Omega; Q = cholqr3(Y); q times
+// { Z = G^T Q; Qhat = cholqr3(Z); Y = G Qhat; Q = cholqr3(Y) }; B = Q^T G.
+#include <math.h>
+
+#include "common.cuh"
+#include "rgsv_internal.h"
+
+namespace rgsv {
+namespace {
+
+constexpr int kTR = 32;       // G rows per streamed tile
+constexpr int kStages = 3;    // cp.async ring depth
+constexpr int kThreads = 256; // 8 warps
+constexpr int kWarps = kThreads / 32;
+
+RGSV_DI uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+RGSV_DI uint32_t cluster_idx() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+RGSV_DI uint32_t cluster_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+RGSV_DI void cluster_barrier() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::
+          : "memory");
+}
+RGSV_DI double ld_dsmem(const double* local, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+  return v;
+}
+RGSV_DI void cp_async16(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+RGSV_DI void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+RGSV_DI void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Y / Z slice layout: row-major, pitch KP doubles, XOR swizzle inside each
+// 16-column group so both DMMA fragment patterns used on it (A: 8 rows x 4
+// cols; B: 4 rows x 8 cols) hit the minimum two shared-memory wavefronts.
+template <int KP>
+RGSV_DI int yx(int r, int c) {
+  return r * KP + ((c & ~15) | ((c & 15) ^ (((r & 1) << 3) | (((r >> 1) & 1) << 2))));
+}
+
+struct ChainArgs {
+  const BatchMat* mats;
+  int nmat;
+  int n;
+  int k;
+  int q;
+  const double* omega;  // per matrix: KP x ldo (Omega^T), stride om_stride
+  int64_t ldo;
+  int64_t om_stride;
+  double* b_out;        // per matrix: KP x ldb, stride b_stride
+  int64_t ldb;
+  int64_t b_stride;
+  double* stats;        // per matrix: {||G||_F^2, ||B||_F^2}
+  int* status;          // per matrix status bits
+  int yrows;            // shared-memory rows of the Y slice (multiple of 32)
+};
+
+template <int NP, int KP>
+struct Layout {
+  static constexpr int GP = NP + 4;                 // G tile pitch (doubles)
+  static constexpr int kG = kStages * kTR * GP;     // G ring
+  static constexpr int kX = KP * GP;                // X^T (KP x NP)
+  static constexpr int kPart = NP * KP;             // one reduction slot
+  static constexpr int kSmall = KP * (KP + 1);      // Gram / L / L^-1
+  static size_t bytes(int yrows) {
+    return sizeof(double) *
+           ((size_t)yrows * KP + kG + kX + 2 * kPart + NP * KP + 3 * kSmall + kWarps * 64 + 64);
+  }
+};
+
+template <int NP, int KP, int CS>
+struct Chain {
+  using Lo = Layout<NP, KP>;
+  static constexpr int GP = Lo::GP;
+  double* ys;    // Y / Q slice (yrows x KP, swizzled)
+  double* gst;   // G tile ring
+  double* xt;    // X^T: KP x GP
+  double* part;  // 2 reduction slots of NP*KP
+  double* zb;    // reduced Z (NP x KP, swizzled like ys)
+  double* gram;  // KP x (KP+1)
+  double* lmat;  // KP x (KP+1): Cholesky factor, in place
+  double* linv;  // KP x (KP+1): L^-1 (row-major)
+  double* wred;  // per-warp partials (kWarps x 64)
+  double* misc;  // scalars
+  int slot;
+  int fail;
+  int tid, lane, warp;
+  uint32_t crank;
+
+  RGSV_DI void init(double* sm, int yrows) {
+    ys = sm;
+    gst = ys + (size_t)yrows * KP;
+    xt = gst + Lo::kG;
+    part = xt + Lo::kX;
+    zb = part + 2 * Lo::kPart;
+    gram = zb + NP * KP;
+    lmat = gram + Lo::kSmall;
+    linv = lmat + Lo::kSmall;
+    wred = linv + Lo::kSmall;
+    misc = wred + kWarps * 64;
+    slot = 0;
+    tid = threadIdx.x;
+    lane = tid & 31;
+    warp = tid >> 5;
+    crank = cluster_rank();
+  }
+
+  // ---- cluster reduction of `cnt` doubles from this CTA's part slot into dst
+  // (every CTA gets the same fixed-order sum). Double-buffered slots make one
+  // cluster barrier per reduction sufficient (see header comment).
+  RGSV_DI double* slot_ptr() { return part + slot * Lo::kPart; }
+  template <typename F>
+  RGSV_DI void reduce(int cnt, F&& store) {
+    double* src = slot_ptr();
+    __syncthreads();
+    cluster_barrier();
+    for (int e = tid; e < cnt; e += kThreads) {
+      double v[CS];
+#pragma unroll
+      for (int r = 0; r < CS; ++r) v[r] = ld_dsmem(src + e, r);  // all loads in flight
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < CS; ++r) s += v[r];  // fixed CTA order
+      store(e, s);
+    }
+    slot ^= 1;
+    __syncthreads();
+  }
+
+  // ---- stream this CTA's G rows [r0, r1) through the ring, tile by tile
+  RGSV_DI void issue_tile(const BatchMat& g, int r0, int r1, int t, int n) {
+    double* dst = gst + (t % kStages) * kTR * GP;
+    constexpr int kChunks = kTR * (NP / 2);
+    for (int e = tid; e < kChunks; e += kThreads) {
+      const int rr = e / (NP / 2), cc = (e % (NP / 2)) * 2;
+      const int row = r0 + t * kTR + rr;
+      int bytes = 0;
+      if (row < r1 && cc < n) bytes = (cc + 1 < n) ? 16 : 8;
+      const double* src = bytes ? g.g + (int64_t)row * g.ld + cc : g.g;
+      cp_async16(dst + rr * GP + cc, src, bytes);
+    }
+  }
+
+  template <typename F>
+  RGSV_DI void stream_g(const BatchMat& g, int r0, int r1, int n, F&& body) {
+    const int rows = r1 - r0;
+    const int T = rows > 0 ? (rows + kTR - 1) / kTR : 0;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+      if (s < T) issue_tile(g, r0, r1, s, n);
+      cp_commit();
+    }
+    for (int t = 0; t < T; ++t) {
+      cp_wait<kStages - 2>();
+      __syncthreads();
+      if (t + kStages - 1 < T) issue_tile(g, r0, r1, t + kStages - 1, n);
+      cp_commit();
+      body(t, gst + (t % kStages) * kTR * GP);
+    }
+    cp_wait<0>();
+    __syncthreads();
+  }
+
+  // ---- Y[t-tile] = G_tile X  (pass A); optional sum of squares of G
+  RGSV_DI void pass_gx(const BatchMat& g, int r0, int r1, int n, double* ss) {
+    constexpr int kRB = kTR / 8, kCB = KP / 8, kBlocks = kRB * kCB;
+    stream_g(g, r0, r1, n, [&](int t, const double* gt) {
+      for (int b = warp; b < kBlocks; b += kWarps) {
+        const int rb = b % kRB, cb = b / kRB;
+        double cc[4][2] = {};
+        const double* arow = gt + (rb * 8 + (lane >> 2)) * GP + (lane & 3);
+        const double* brow = xt + (cb * 8 + (lane >> 2)) * GP + (lane & 3);
+#pragma unroll
+        for (int ks = 0; ks < NP / 4; ks += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(cc[u], arow[(ks + u) * 4], brow[(ks + u) * 4]);
+        }
+        double c[2] = {(cc[0][0] + cc[1][0]) + (cc[2][0] + cc[3][0]),
+                       (cc[0][1] + cc[1][1]) + (cc[2][1] + cc[3][1])};
+        const int r = t * kTR + rb * 8 + (lane >> 2);
+        const int col = cb * 8 + 2 * (lane & 3);
+        ys[yx<KP>(r, col)] = c[0];
+        ys[yx<KP>(r, col + 1)] = c[1];
+      }
+      if (ss) {
+        double a = 0.0;
+        for (int e = tid; e < kTR * NP; e += kThreads) {
+          const double v = gt[(e / NP) * GP + (e % NP)];
+          a = fma(v, v, a);
+        }
+        *ss += a;
+      }
+    });
+  }
+
+  // ---- part = G^T Y over this CTA's rows (pass B), NP x KP
+  RGSV_DI void pass_gtq(const BatchMat& g, int r0, int r1, int n) {
+    constexpr int kIB = NP / 8, kJB = KP / 8, kBlocks = kIB * kJB;
+    constexpr int kPer = (kBlocks + kWarps - 1) / kWarps;
+    double acc[kPer][2][2] = {};
+    stream_g(g, r0, r1, n, [&](int t, const double* gt) {
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int b = warp + i * kWarps;
+        if (b >= kBlocks) break;
+        const int ib = b % kIB, jb = b / kIB;
+#pragma unroll
+        for (int ks = 0; ks < kTR / 4; ++ks) {
+          const int rr = ks * 4 + (lane & 3);
+          const double a = gt[rr * GP + ib * 8 + (lane >> 2)];
+          const double bv = ys[yx<KP>(t * kTR + rr, jb * 8 + (lane >> 2))];
+          dmma(acc[i][ks & 1], a, bv);
+        }
+      }
+    });
+    double* dst = slot_ptr();
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int b = warp + i * kWarps;
+      if (b >= kBlocks) break;
+      const int ib = b % kIB, jb = b / kIB;
+      const int r = ib * 8 + (lane >> 2), c = jb * 8 + 2 * (lane & 3);
+      dst[r * KP + c] = acc[i][0][0] + acc[i][1][0];
+      dst[r * KP + c + 1] = acc[i][0][1] + acc[i][1][1];
+    }
+  }
+
+  // ---- Gram of a swizzled slice buf (rows x KP) into this CTA's part slot
+  RGSV_DI void gram_partial(const double* buf, int rows) {
+    constexpr int kB = (KP / 8) * (KP / 8);
+    const int nks = (rows + 3) / 4;
+    double* dst = slot_ptr();
+    if (kB >= kWarps) {
+      for (int b = warp; b < kB; b += kWarps) {
+        const int ib = b % (KP / 8), jb = b / (KP / 8);
+        double c[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+        int ks = 0;
+        for (; ks + 1 < nks; ks += 2) {
+          const int rr = ks * 4 + (lane & 3);
+          dmma(c, buf[yx<KP>(rr, ib * 8 + (lane >> 2))], buf[yx<KP>(rr, jb * 8 + (lane >> 2))]);
+          dmma(c2, buf[yx<KP>(rr + 4, ib * 8 + (lane >> 2))],
+               buf[yx<KP>(rr + 4, jb * 8 + (lane >> 2))]);
+        }
+        if (ks < nks) {
+          const int rr = ks * 4 + (lane & 3);
+          dmma(c, buf[yx<KP>(rr, ib * 8 + (lane >> 2))], buf[yx<KP>(rr, jb * 8 + (lane >> 2))]);
+        }
+        c[0] += c2[0];
+        c[1] += c2[1];
+        const int r = ib * 8 + (lane >> 2), col = jb * 8 + 2 * (lane & 3);
+        dst[r * KP + col] = c[0];
+        dst[r * KP + col + 1] = c[1];
+      }
+      return;
+    }
+    // kB = 4 (KP = 16): warp -> block (warp % 4), k-steps split by warp / 4
+    const int b = warp % kB, half = warp / kB;
+    const int ib = b % (KP / 8), jb = b / (KP / 8);
+    constexpr int kStep = kWarps / kB;
+    double c[4][2] = {};
+    int ks = half;
+    for (; ks + 3 * kStep < nks; ks += 4 * kStep) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = (ks + u * kStep) * 4 + (lane & 3);
+        dmma(c[u], buf[yx<KP>(rr, ib * 8 + (lane >> 2))], buf[yx<KP>(rr, jb * 8 + (lane >> 2))]);
+      }
+    }
+    for (; ks < nks; ks += kStep) {
+      const int rr = ks * 4 + (lane & 3);
+      dmma(c[0], buf[yx<KP>(rr, ib * 8 + (lane >> 2))], buf[yx<KP>(rr, jb * 8 + (lane >> 2))]);
+    }
+    c[0][0] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+    c[0][1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
+    wred[warp * 64 + lane * 2] = c[0][0];
+    wred[warp * 64 + lane * 2 + 1] = c[0][1];
+    __syncthreads();
+    if (warp < kB) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int h = 0; h < kWarps / kB; ++h) {  // fixed order
+        s0 += wred[(warp + h * kB) * 64 + lane * 2];
+        s1 += wred[(warp + h * kB) * 64 + lane * 2 + 1];
+      }
+      const int r = ib * 8 + (lane >> 2), col = jb * 8 + 2 * (lane & 3);
+      dst[r * KP + col] = s0;
+      dst[r * KP + col + 1] = s1;
+    }
+  }
+
+  // ---- shifted Cholesky of gram (k x k) -> linv = L^-1; identity on the
+  //      padding. One warp, register resident (lane i holds row i; columns
+  //      are compile-time indices). Symmetric Gauss-Jordan: eliminating below
+  //      pivot j with row operations turns [A | I] into [D Lhat^T | Lhat^-1];
+  //      scaling row j by d_j^-1/2 makes the right half L^-1, so the inverse
+  //      needs no separate substitution sweep. Row j is broadcast by
+  //      independent shuffles; the critical path per step is one shuffle,
+  //      one rsqrt and one FMA.
+  RGSV_DI void chol(int k, int64_t shift_rows) {
+    constexpr int LD = KP + 1;
+    static_assert(KP <= 32, "one lane per row");
+    if (warp == 0) {
+      const bool row_ok = lane < k;
+      double a[KP], x[KP];
+#pragma unroll
+      for (int c = 0; c < KP; ++c) {
+        a[c] = (row_ok && c < k) ? gram[lane * LD + c] : (lane == c ? 1.0 : 0.0);
+        x[c] = (lane == c) ? 1.0 : 0.0;
+      }
+      if (shift_rows > 0) {
+        double dg = 0.0;
+#pragma unroll
+        for (int c = 0; c < KP; ++c)
+          if (c == lane && row_ok) dg = a[c];
+        const double tr = warp_sum(dg);
+        const double sh = 11.0 * ((double)shift_rows * k + (double)k * (k + 1)) * 0x1p-53 * tr;
+#pragma unroll
+        for (int c = 0; c < KP; ++c)
+          if (c == lane && row_ok) a[c] += sh;
+      }
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < KP; ++j) {
+        const double d = __shfl_sync(0xffffffffu, a[j], j);
+        double pa[KP], px[KP];
+#pragma unroll
+        for (int c = 0; c < KP; ++c) {
+          if (c > j) pa[c] = __shfl_sync(0xffffffffu, a[c], j);
+          if (c <= j) px[c] = __shfl_sync(0xffffffffu, x[c], j);
+        }
+        bad |= !(d > 0.0) || !isfinite(d);
+        const double r = rsqrt(d);
+        const double f = a[j] * (r * r);  // A[i][j] / d
+        if (lane > j) {
+#pragma unroll
+          for (int c = 0; c < KP; ++c) {
+            if (c > j) a[c] = fma(-f, pa[c], a[c]);
+            if (c <= j) x[c] = fma(-f, px[c], x[c]);
+          }
+          a[j] = 0.0;
+        } else if (lane == j) {
+#pragma unroll
+          for (int c = 0; c < KP; ++c) {
+            if (c > j) a[c] *= r;
+            if (c <= j) x[c] *= r;
+          }
+          a[j] = d * r;
+        }
+      }
+      if (bad) fail = 1;
+      if (lane < KP) {
+#pragma unroll
+        for (int c = 0; c < KP; ++c)
+          linv[lane * LD + c] = bad ? (lane == c ? 1.0 : 0.0) : (c <= lane ? x[c] : 0.0);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- buf (rows x KP, swizzled) <- buf L^-T, in place, warp per 8 rows
+  RGSV_DI void trsm(double* buf, int rows) {
+    constexpr int LD = KP + 1;
+    const int nrb = (rows + 7) / 8;
+    for (int rb = warp; rb < nrb; rb += kWarps) {
+      const int r = rb * 8 + (lane >> 2);
+      double a[KP / 4];
+#pragma unroll
+      for (int ks = 0; ks < KP / 4; ++ks) a[ks] = buf[yx<KP>(r, ks * 4 + (lane & 3))];
+      __syncwarp();
+#pragma unroll
+      for (int cb = 0; cb < KP / 8; ++cb) {
+        double c[2] = {0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < KP / 4; ++ks)
+          dmma(c, a[ks], linv[(cb * 8 + (lane >> 2)) * LD + ks * 4 + (lane & 3)]);
+        const int col = cb * 8 + 2 * (lane & 3);
+        buf[yx<KP>(r, col)] = c[0];
+        buf[yx<KP>(r, col + 1)] = c[1];
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- shifted CholeskyQR3 of a row-sharded slice (cluster Gram) or of a
+  //      replicated small matrix (local Gram, no cluster traffic)
+  RGSV_DI void cholqr3(double* buf, int rows, int k, int64_t shift_rows, bool sharded) {
+    constexpr int LD = KP + 1;
+    for (int pass = 0; pass < 3; ++pass) {
+      gram_partial(buf, rows);
+      if (sharded) {
+        reduce(KP * KP, [&](int e, double s) { gram[(e / KP) * LD + (e % KP)] = s; });
+      } else {
+        __syncthreads();
+        const double* src = slot_ptr();
+        for (int e = tid; e < KP * KP; e += kThreads) gram[(e / KP) * LD + (e % KP)] = src[e];
+        __syncthreads();
+      }
+      chol(k, pass == 0 ? shift_rows : 0);
+      trsm(buf, rows);
+    }
+  }
+};
+
+template <int NP, int KP, int CS>
+__global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
+  extern __shared__ __align__(16) double smc[];
+  Chain<NP, KP, CS> C;
+  C.init(smc, A.yrows);
+  constexpr int LD = KP + 1;
+  const int n = A.n, k = A.k;
+  for (int mat = cluster_idx(); mat < A.nmat; mat += cluster_count()) {
+    const BatchMat g = A.mats[mat];
+    const int rows = g.rows;
+    const int rpc = (rows + CS - 1) / CS;
+    const int r0 = min(rows, (int)C.crank * rpc), r1 = min(rows, r0 + rpc);
+    const int rl = r1 - r0;
+    const int rl32 = (rl + kTR - 1) / kTR * kTR;
+    C.fail = 0;
+    // X^T = Omega^T block (KP x n), zero-padded
+    const double* om = A.omega + (int64_t)mat * A.om_stride;
+    for (int e = C.tid; e < KP * NP; e += kThreads) {
+      const int i = e / NP, j = e % NP;
+      C.xt[i * C.GP + j] = (i < k && j < n) ? om[(int64_t)i * A.ldo + j] : 0.0;
+    }
+    for (int e = C.tid; e < A.yrows * KP; e += kThreads) C.ys[e] = 0.0;
+    __syncthreads();
+    // (1) sketch Y = G Omega, ||G||^2 on the side
+    double ss = 0.0;
+    C.pass_gx(g, r0, r1, n, &ss);
+    __syncthreads();
+    // ||G||_F^2: block partial in fixed order -> cluster sum
+    {
+      double v = warp_sum(ss);
+      if (C.lane == 0) C.wred[C.warp * 64] = v;
+      __syncthreads();
+      if (C.tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s += C.wred[w * 64];
+        C.slot_ptr()[0] = s;
+      }
+      C.reduce(1, [&](int, double s) { C.misc[0] = s; });
+    }
+    C.cholqr3(C.ys, rl32, k, rows, true);
+    for (int it = 0; it < A.q; ++it) {
+      // (2) Z = G^T Q (n x k), cluster-reduced, then Qhat = cholqr3(Z)
+      C.pass_gtq(g, r0, r1, n);
+      C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
+      C.cholqr3(C.zb, NP, k, n, false);
+      for (int e = C.tid; e < KP * NP; e += kThreads) {
+        const int i = e / NP, j = e % NP;
+        C.xt[i * C.GP + j] = (j < n) ? C.zb[yx<KP>(j, i)] : 0.0;
+      }
+      __syncthreads();
+      // (3) Y = G Qhat, Q = cholqr3(Y)
+      C.pass_gx(g, r0, r1, n, nullptr);
+      __syncthreads();
+      C.cholqr3(C.ys, rl32, k, rows, true);
+    }
+    // (4) B^T = G^T Q (n x k), cluster-reduced; rank 0 writes B and ||B||^2
+    C.pass_gtq(g, r0, r1, n);
+    C.reduce(NP * KP, [&](int e, double s) { C.zb[e] = s; });
+    if (C.crank == 0) {
+      double* bo = A.b_out + (int64_t)mat * A.b_stride;
+      double e2 = 0.0;
+      for (int e = C.tid; e < KP * n; e += kThreads) {
+        const int i = e / n, j = e % n;
+        const double v = (i < k) ? C.zb[j * KP + i] : 0.0;
+        bo[(int64_t)i * A.ldb + j] = v;
+        e2 = fma(v, v, e2);
+      }
+      e2 = warp_sum(e2);
+      if (C.lane == 0) C.wred[C.warp * 64 + 1] = e2;
+      __syncthreads();
+      if (C.tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s += C.wred[w * 64 + 1];
+        A.stats[2 * mat] = C.misc[0];
+        A.stats[2 * mat + 1] = s;
+        int st = C.fail ? RGSV_ST_CHOL_BREAKDOWN : 0;
+        if (!isfinite(C.misc[0])) st |= RGSV_ST_NONFINITE;
+        A.status[mat] = st;
+      }
+    }
+    (void)LD;
+    __syncthreads();
+  }
+  cluster_barrier();  // no CTA leaves while a peer may still read its slots
+}
+
+template <int NP, int KP, int CS>
+int launch_chain_t(const ChainArgs& a, cudaStream_t st) {
+  const size_t smem = Layout<NP, KP>::bytes(a.yrows);
+  if (smem > 227 * 1024) return RGSV_ERR_DIMENSION;
+  auto kern = k_batch_chain<NP, KP, CS>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return RGSV_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent clusters: exactly as many as can be co-resident, otherwise the
+  // clusters that do not fit would run their whole matrix list afterwards
+  static int resident[4] = {0, 0, 0, 0};
+  int& clusters_max = resident[CS == 1 ? 0 : CS == 2 ? 1 : CS == 4 ? 2 : 3];
+  if (clusters_max == 0) {
+    cfg.gridDim = dim3(kSMs / CS * CS, 1, 1);
+    if (cudaOccupancyMaxActiveClusters(&clusters_max, (void*)kern, &cfg) != cudaSuccess ||
+        clusters_max < 1)
+      clusters_max = kSMs / CS;
+  }
+  int clusters = clusters_max;
+  if (clusters > a.nmat) clusters = a.nmat;
+  cfg.gridDim = dim3(clusters * CS, 1, 1);
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return RGSV_ERR_CUDA;
+  note_launch();
+  return 0;
+}
+
+template <int NP, int KP>
+int launch_chain_np(const ChainArgs& a, int cs, cudaStream_t st) {
+  switch (cs) {
+    case 1: return launch_chain_t<NP, KP, 1>(a, st);
+    case 2: return launch_chain_t<NP, KP, 2>(a, st);
+    case 4: return launch_chain_t<NP, KP, 4>(a, st);
+    case 8: return launch_chain_t<NP, KP, 8>(a, st);
+  }
+  return RGSV_ERR_DIMENSION;
+}
+
+}  // namespace
+
+// Cluster size and Y-slice rows for a batch: the smallest portable cluster
+// whose per-CTA slice fits the shared-memory budget.
+int batch_chain_plan(int max_rows, int n, int k, int* cs_out, int* yrows_out) {
+  const int kp = k <= 16 ? 16 : 32;
+  const int np = n <= 64 ? 64 : 128;
+  if (k < 1 || k > 32 || n < 1 || n > 128 || k > n) return RGSV_ERR_DIMENSION;
+  for (int cs = 1; cs <= 8; cs *= 2) {
+    const int rpc = (max_rows + cs - 1) / cs;
+    const int yrows = (rpc + kTR - 1) / kTR * kTR;
+    size_t bytes;
+    if (np == 64) bytes = kp == 16 ? Layout<64, 16>::bytes(yrows) : Layout<64, 32>::bytes(yrows);
+    else bytes = kp == 16 ? Layout<128, 16>::bytes(yrows) : Layout<128, 32>::bytes(yrows);
+    if (bytes <= 227 * 1024) {
+      *cs_out = cs;
+      *yrows_out = yrows;
+      return 0;
+    }
+  }
+  return RGSV_ERR_DIMENSION;
+}
+
+int batch_chain(const BatchMat* mats, int nmat, int max_rows, int n, int k, int q,
+                const double* omega, int64_t ldo, int64_t om_stride, double* b_out, int64_t ldb,
+                int64_t b_stride, double* stats, int* status, cudaStream_t st) {
+  int cs, yrows;
+  if (int e = batch_chain_plan(max_rows, n, k, &cs, &yrows)) return e;
+  ChainArgs a{mats, nmat, n, k, q, omega, ldo, om_stride, b_out, ldb, b_stride, stats, status,
+              yrows};
+  const int kp = k <= 16 ? 16 : 32;
+  if (n <= 64) return kp == 16 ? launch_chain_np<64, 16>(a, cs, st) : launch_chain_np<64, 32>(a, cs, st);
+  return kp == 16 ? launch_chain_np<128, 16>(a, cs, st) : launch_chain_np<128, 32>(a, cs, st);
+}
+
+}  // namespace rgsv

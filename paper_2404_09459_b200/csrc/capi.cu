@@ -206,6 +206,73 @@ int rgsv_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, in
   return launch_axpy(y, ldy, x, ldx, rows, cols, alpha, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------- batched
+namespace {
+struct BatchLayout {
+  size_t omega, omega_ws, omega_ws_bytes, b, mstat, total;
+  int64_t kp, ldo;
+};
+BatchLayout batch_layout(int npairs, int64_t n, int k) {
+  BatchLayout L{};
+  L.kp = k <= 16 ? 16 : 32;
+  L.ldo = ceil16(n);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = al256(off + bytes);
+    return o;
+  };
+  const int nm = 2 * npairs;
+  L.omega = take((size_t)nm * L.kp * L.ldo * 8);
+  L.omega_ws_bytes = rgsv::omega_workspace_bytes(nm, n * (int64_t)k);
+  L.omega_ws = take(L.omega_ws_bytes);
+  L.b = take((size_t)nm * L.kp * L.ldo * 8);
+  L.mstat = take((size_t)nm * 4);
+  L.total = off;
+  return L;
+}
+}  // namespace
+
+int rgsv_batch_supported(int max_rows, int64_t n, int k) {
+  int cs, yrows;
+  if (n > 128 || 2 * k > n || k < 1 || max_rows < k) return 0;
+  return rgsv::batch_chain_plan(max_rows, (int)n, k, &cs, &yrows) == 0 ? 1 : 0;
+}
+
+size_t rgsv_batch_workspace_bytes(int npairs, int64_t n, int k) {
+  return batch_layout(npairs, n, k).total;
+}
+
+int rgsv_batch_gsvd(const void* mats, int npairs, int max_rows, int64_t n, int k, int q,
+                    const uint64_t* seeds, double classify_tol, double* res, int* ints,
+                    double* stats, int* status, double* b_out, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (npairs < 1 || k < 1 || k > 32 || n < 2 * k || n > 128 || q < 0 || max_rows < k)
+    return RGSV_ERR_DIMENSION;
+  if (!(classify_tol > 0.0 && classify_tol < 1e-2)) return RGSV_ERR_VALIDATION;
+  BatchLayout L = batch_layout(npairs, n, k);
+  if (workspace_bytes < L.total) return RGSV_ERR_WORKSPACE;
+  char* ws = static_cast<char*>(workspace);
+  double* om = reinterpret_cast<double*>(ws + L.omega);
+  double* b = b_out ? b_out : reinterpret_cast<double*>(ws + L.b);
+  int* mstat = reinterpret_cast<int*>(ws + L.mstat);
+  const int nm = 2 * npairs;
+  if (cudaMemsetAsync(om, 0, (size_t)nm * L.kp * L.ldo * 8, st) != cudaSuccess) return RGSV_ERR_CUDA;
+  if (cudaMemsetAsync(status, 0, (size_t)npairs * 4, st) != cudaSuccess) return RGSV_ERR_CUDA;
+  // Omega_i for every matrix from its own stream (pair j: seeds 2j, 2j+1)
+  if (int e = rgsv::omega_generate(seeds, nm, n, k, om, L.ldo, L.kp * L.ldo, status,
+                                   ws + L.omega_ws, L.omega_ws_bytes, st))
+    return e;
+  if (int e = rgsv::batch_chain(static_cast<const rgsv::BatchMat*>(mats), nm, max_rows, (int)n, k,
+                                q, om, L.ldo, L.kp * L.ldo, b, L.ldo, L.kp * L.ldo, stats, mstat,
+                                st))
+    return e;
+  const int64_t res_stride = 6 * n + 4 + 2 * k;
+  return rgsv::launch_batch_small(b, L.ldo, L.kp * L.ldo, npairs, k, k, (int)n, classify_tol, res,
+                                  res_stride, ints, status, mstat, st);
+}
+
 size_t rgsv_sketch_workspace_bytes(int64_t m, int64_t n, int k) {
   return sketch_layout(m, n, k).total;
 }

@@ -38,6 +38,22 @@ int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv
 int chol_profile(const double* gram, int k, int kp, double* linv, long long* prof, int* status,
                  cudaStream_t st);
 
+// batched small-pair chains (batch.cu)
+struct BatchMat {
+  const double* g;
+  int64_t ld;
+  int rows;
+  int pad;
+};
+int batch_chain_plan(int max_rows, int n, int k, int* cs_out, int* yrows_out);
+int batch_chain(const BatchMat* mats, int nmat, int max_rows, int n, int k, int q,
+                const double* omega, int64_t ldo, int64_t om_stride, double* b_out, int64_t ldb,
+                int64_t b_stride, double* stats, int* status, cudaStream_t st);
+
+int launch_batch_small(const double* b, int64_t ldb, int64_t b_stride, int npairs, int k1, int k2,
+                       int n, double tol, double* res, int64_t res_stride, int* ints,
+                       int* status, const int* mat_status, cudaStream_t st);
+
 size_t omega_workspace_bytes(int nstreams, int64_t nvals);
 int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double* out,
                    int64_t ldo, int64_t out_stride, int* status, void* ws, size_t ws_bytes,

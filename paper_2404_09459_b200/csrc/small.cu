@@ -59,24 +59,16 @@ RGSV_DI int rr_index(int p, int round, int nplayers) {
 
 constexpr int kJacobiMaxVec = 2048;
 
-__global__ void __launch_bounds__(1024) k_jacobi_rows(JacobiJob j0, JacobiJob j1, int max_sweeps,
-                                                       int* __restrict__ status, int use_smem) {
-  JacobiJob J = blockIdx.x == 0 ? j0 : j1;
+// One-sided Jacobi on the rows of J.v (in place), whole CTA; writes the
+// sorted singular values and their count. Shared by k_jacobi_rows and the
+// batched small-GSVD kernel.
+__device__ void jacobi_rows_body(JacobiJob J, int max_sweeps, int* __restrict__ status) {
   __shared__ double nrm[kJacobiMaxVec];
-  extern __shared__ double jsm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int nout = J.nv < J.len ? J.nv : J.len;
   if (J.nv <= 0 || J.len <= 0) {
     if (tid == 0) *J.nsv_out = 0;
     return;
-  }
-  if (use_smem) {  // stage the vectors in shared memory (ld len + 1)
-    const int lds = J.len + 1;
-    for (int i = warp; i < J.nv; i += nwarps)
-      for (int e = lane; e < J.len; e += 32) jsm[i * lds + e] = J.v[(int64_t)i * J.ld + e];
-    J.v = jsm;
-    J.ld = lds;
-    __syncthreads();
   }
   const int nve = J.nv + (J.nv & 1);
   const double tol = fmax(1e-15, sqrt((double)J.len) * 2.220446049250313e-16);
@@ -136,6 +128,23 @@ __global__ void __launch_bounds__(1024) k_jacobi_rows(JacobiJob j0, JacobiJob j1
     if (rank < nout) J.sv_out[rank] = x;
   }
   if (tid == 0) *J.nsv_out = nout;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) k_jacobi_rows(JacobiJob j0, JacobiJob j1, int max_sweeps,
+                                                       int* __restrict__ status, int use_smem) {
+  JacobiJob J = blockIdx.x == 0 ? j0 : j1;
+  extern __shared__ double jsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  if (use_smem && J.nv > 0 && J.len > 0) {  // stage the vectors in shared memory (ld len + 1)
+    const int lds = J.len + 1;
+    for (int i = warp; i < J.nv; i += nwarps)
+      for (int e = lane; e < J.len; e += 32) jsm[i * lds + e] = J.v[(int64_t)i * J.ld + e];
+    J.v = jsm;
+    J.ld = lds;
+    __syncthreads();
+  }
+  jacobi_rows_body(J, max_sweeps, status);
 }
 
 // ------------------------------------------- Jacobi SVD with vectors
@@ -281,17 +290,13 @@ int launch_scale_cols(double* a, int64_t lda, int rows, int cols, const double* 
 // v^T with v[0] = 1) then dorg2r (backward accumulation of Q = H0 .. H_{l-1}).
 // Column signs of Q may differ from the reference's phase fix
 // (core.py:88-95); singular values of its row blocks do not depend on them.
-template <bool SMEM>
-__global__ void __launch_bounds__(512) k_householder_small(const double* __restrict__ b1,
-                                                           int64_t ld1, int l1,
-                                                           const double* __restrict__ b2,
-                                                           int64_t ld2, int l2,
-                                                           double* __restrict__ q, int64_t ldq,
-                                                           double* __restrict__ gwork) {
-  extern __shared__ double smh[];
+// Q of the l x l block in A (lda = l + 1; loaded from the first l columns of
+// [B1; B2]), in place; copied to q when q != nullptr. Whole CTA.
+__device__ void hh_small_body(const double* __restrict__ b1, int64_t ld1, int l1,
+                              const double* __restrict__ b2, int64_t ld2, int l2,
+                              double* __restrict__ q, int64_t ldq, double* A) {
   const int l = l1 + l2;
   const int lda = l + 1;
-  double* A = SMEM ? smh : gwork;  // l x lda: T -> R + reflectors -> Q (in place)
   __shared__ double w[512];
   __shared__ double tau[512];
   __shared__ double s_beta, s_scale, s_tau;
@@ -383,8 +388,21 @@ __global__ void __launch_bounds__(512) k_householder_small(const double* __restr
     }
     __syncthreads();
   }
-  for (int i = warp; i < l; i += nwarp)
-    for (int j = lane; j < l; j += 32) q[(int64_t)i * ldq + j] = A[i * lda + j];
+  if (q)
+    for (int i = warp; i < l; i += nwarp)
+      for (int j = lane; j < l; j += 32) q[(int64_t)i * ldq + j] = A[i * lda + j];
+  __syncthreads();
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(512) k_householder_small(const double* __restrict__ b1,
+                                                           int64_t ld1, int l1,
+                                                           const double* __restrict__ b2,
+                                                           int64_t ld2, int l2,
+                                                           double* __restrict__ q, int64_t ldq,
+                                                           double* __restrict__ gwork) {
+  extern __shared__ double smh[];
+  hh_small_body(b1, ld1, l1, b2, ld2, l2, q, ldq, SMEM ? smh : gwork);
 }
 
 // Register-resident variant for l <= 128: warp w owns columns c = w, w+16,
@@ -774,6 +792,14 @@ __device__ double block_sum(double v, double* red) {
 // mode 1: from a given spectrum (sv1 = alphas, sv2 = betas, r = r_given);
 // mode 2: entropy of a given probability vector sv1 (scalars[0] = D,
 //         scalars[2] = sum p).
+__device__ void comparative_body(const double* __restrict__ sv1, const int* __restrict__ nsv,
+                                 const double* __restrict__ sv2, int64_t n, double tol,
+                                 double* __restrict__ A, double* __restrict__ B,
+                                 double* __restrict__ rho, double* __restrict__ theta,
+                                 double* __restrict__ p1, double* __restrict__ p2,
+                                 double* __restrict__ scalars, int* __restrict__ counts,
+                                 int* __restrict__ status, double* red);
+
 __global__ void __launch_bounds__(1024) k_comparative(
     const double* __restrict__ sv1, const int* __restrict__ nsv, const double* __restrict__ sv2,
     int64_t n, double tol, double* __restrict__ A, double* __restrict__ B,
@@ -838,6 +864,19 @@ __global__ void __launch_bounds__(1024) k_comparative(
     }
     return;
   }
+  comparative_body(sv1, nsv, sv2, n, tol, A, B, rho, theta, p1, p2, scalars, counts, status, red);
+}
+
+// spectrum completion + classification + comparative quantities (mode 0 of
+// k_comparative); whole CTA, `red` = 32 doubles of shared scratch.
+__device__ void comparative_body(const double* __restrict__ sv1, const int* __restrict__ nsv,
+                                 const double* __restrict__ sv2, int64_t n, double tol,
+                                 double* __restrict__ A, double* __restrict__ B,
+                                 double* __restrict__ rho, double* __restrict__ theta,
+                                 double* __restrict__ p1, double* __restrict__ p2,
+                                 double* __restrict__ scalars, int* __restrict__ counts,
+                                 int* __restrict__ status, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t c1 = nsv[0], c2 = nsv[1];
   double cr = 0.0, cza = 0.0;
   for (int64_t i = tid; i < n; i += nt) {
@@ -925,6 +964,69 @@ __global__ void __launch_bounds__(1024) k_comparative(
     if (n < 2 || fabs(s1 - 1.0) > 1e-10 || fabs(s2 - 1.0) > 1e-10)
       atomicOr(status, RGSV_ST_NOT_NORMALIZED);
   }
+}
+
+// ------------------------------------------------- batched small GSVD
+// One CTA per pair j: stacked QR of [B1_j; B2_j] (k1 + k2 = l <= n, so the
+// Q of the leading l x l block, engine.py:257), Jacobi singular values of
+// L1 = Q[:k1] and L2 = Q[k1:] (engine.py:228-231), then the spectrum /
+// classification / comparative kernel body (engine.py:189-225,
+// analysis.py:37-102) -- all in shared memory, one launch for the batch.
+// Per pair outputs: res[j] = {alphas, betas, rho, theta, p1, p2 (n each),
+// scalars (4), sv1 (k1), sv2 (k2)}, ints[j] = {nsv1, nsv2, r, s},
+// status[j] |= bits.
+__global__ void __launch_bounds__(256) k_batch_small(const double* __restrict__ b, int64_t ldb,
+                                                     int64_t b_stride, int k1, int k2, int n,
+                                                     double tol, double* __restrict__ res,
+                                                     int64_t res_stride, int* __restrict__ ints,
+                                                     int* __restrict__ status,
+                                                     const int* __restrict__ mat_status) {
+  extern __shared__ double sbs[];
+  __shared__ double red[32];
+  __shared__ double sv[128];
+  __shared__ int nsv[2];
+  const int j = blockIdx.x;
+  const int l = k1 + k2;
+  const double* b1 = b + (int64_t)(2 * j) * b_stride;
+  const double* b2 = b + (int64_t)(2 * j + 1) * b_stride;
+  double* A = sbs;  // l x (l + 1)
+  hh_small_body(b1, ldb, k1, b2, ldb, k2, nullptr, 0, A);
+  int* st = status + j;
+  if (threadIdx.x == 0 && mat_status) atomicOr(st, mat_status[2 * j] | mat_status[2 * j + 1]);
+  JacobiJob J1{A, l + 1, k1, l, sv, nsv};
+  jacobi_rows_body(J1, 60, st);
+  JacobiJob J2{A + (int64_t)k1 * (l + 1), l + 1, k2, l, sv + 64, nsv + 1};
+  jacobi_rows_body(J2, 60, st);
+  double* o = res + (int64_t)j * res_stride;
+  comparative_body(sv, nsv, sv + 64, n, tol, o, o + n, o + 2 * n, o + 3 * n, o + 4 * n,
+                   o + 5 * n, o + 6 * n, ints + 4 * j + 2, st, red);
+  __syncthreads();
+  for (int i = threadIdx.x; i < k1; i += blockDim.x) o[6 * n + 4 + i] = sv[i];
+  for (int i = threadIdx.x; i < k2; i += blockDim.x) o[6 * n + 4 + k1 + i] = sv[64 + i];
+  if (threadIdx.x == 0) {
+    ints[4 * j] = nsv[0];
+    ints[4 * j + 1] = nsv[1];
+  }
+}
+
+int launch_batch_small(const double* b, int64_t ldb, int64_t b_stride, int npairs, int k1, int k2,
+                       int n, double tol, double* res, int64_t res_stride, int* ints,
+                       int* status, const int* mat_status, cudaStream_t st) {
+  const int l = k1 + k2;
+  if (npairs < 1 || k1 < 1 || k2 < 1 || k1 > 64 || k2 > 64 || l > n || l > 128)
+    return RGSV_ERR_DIMENSION;
+  const size_t smem = (size_t)l * (l + 1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_batch_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             140 * 1024) != cudaSuccess)
+      return RGSV_ERR_CUDA;
+    attr = true;
+  }
+  k_batch_small<<<npairs, 256, smem, st>>>(b, ldb, b_stride, k1, k2, n, tol, res, res_stride, ints,
+                                           status, mat_status);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
 // ------------------------------------------------------------- sum of squares

@@ -453,3 +453,93 @@ def device_sumsq(g: DevMatrix) -> float:
 
 __all__ = ["DevMatrix", "to_device", "pair_plan", "PairPlan", "SketchPlan", "omega_device",
            "residual_history", "device_sumsq", "ceil16", "_native"]
+
+
+# ------------------------------------------------------- many small pairs
+_DESC = np.dtype([("g", "<u8"), ("ld", "<i8"), ("rows", "<i4"), ("pad", "<i4")])
+
+
+def small_batch_fits(max_rows: int, n: int, k1: int, k2: int) -> bool:
+    """Shapes served by rgsv_batch_gsvd (the cfg3 kernels)."""
+    return k1 == k2 and bool(lib().rgsv_batch_supported(max_rows, n, k1))
+
+
+class SmallBatchPlan:
+    """rgsv_batch_gsvd for B same-shape small pairs: descriptors, workspace
+    and outputs live in HBM across calls; one packed D2H per run."""
+
+    def __init__(self, B: int, n: int, k: int):
+        require_device()
+        self.B, self.n, self.k = B, n, k
+        L = lib()
+        self.ws_bytes = int(L.rgsv_batch_workspace_bytes(B, n, k))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
+        self.res_stride = 6 * n + 4 + 2 * k
+        # res | stats, one float64 buffer; ints | status, one int32 buffer
+        self.fbuf = torch.zeros(B * self.res_stride + 4 * B, dtype=F64, device="cuda")
+        self.ibuf = torch.zeros(5 * B, dtype=torch.int32, device="cuda")
+        self.fhost = torch.empty(self.fbuf.shape, dtype=F64, pin_memory=True)
+        self.ihost = torch.empty(self.ibuf.shape, dtype=torch.int32, pin_memory=True)
+        self.desc = torch.zeros(2 * B * _DESC.itemsize, dtype=torch.uint8, device="cuda")
+        self.seeds = torch.zeros(2 * B, dtype=torch.int64, device="cuda")
+        self._desc_key = None
+        self._seed_key = None
+
+    def set_pairs(self, pairs) -> int:
+        """Descriptors {G1_j, G2_j} of the (resident) pairs; returns max rows."""
+        mats = []
+        for g1, g2 in pairs:
+            mats += [g1, g2]
+        key = tuple((g.t.data_ptr(), g.ld, g.rows) for g in mats)
+        if key != self._desc_key:
+            arr = np.zeros(len(mats), dtype=_DESC)
+            arr["g"] = [g.t.data_ptr() for g in mats]
+            arr["ld"] = [g.ld for g in mats]
+            arr["rows"] = [g.rows for g in mats]
+            self.desc.copy_(torch.from_numpy(arr.view(np.uint8)))
+            self._desc_key = key
+            self.max_rows = max(g.rows for g in mats)
+        return self.max_rows
+
+    def set_seeds(self, seeds) -> None:
+        key = tuple(seeds)
+        if key != self._seed_key:
+            words = []
+            for s in seeds:  # G1: seed, G2: seed + 1 (engine.py:252-253)
+                words += [seed_word(s), seed_word(int(s) + 1)]
+            self.seeds.copy_(torch.tensor(words, dtype=torch.int64))
+            self._seed_key = key
+
+    def launch(self, q_iters: int, classify_tol: float, stream=None, b_out=None) -> None:
+        """b_out: optional (2B x kp x ceil16(n)) tensor receiving every B."""
+        st = stream or torch.cuda.current_stream()
+        B, n, k = self.B, self.n, self.k
+        res = self.fbuf[: B * self.res_stride]
+        stats = self.fbuf[B * self.res_stride:]
+        bo = vp(b_out) if b_out is not None else ctypes.c_void_p(0)
+        check(lib().rgsv_batch_gsvd(vp(self.desc), B, self.max_rows, n, k, q_iters,
+                                    vp(self.seeds), float(classify_tol), vp(res),
+                                    vp(self.ibuf[: 4 * B]), vp(stats), vp(self.ibuf[4 * B:]), bo,
+                                    vp(self.ws), self.ws_bytes, sp(st)), "rgsv_batch_gsvd")
+
+    def fetch(self):
+        self.fhost.copy_(self.fbuf, non_blocking=True)
+        self.ihost.copy_(self.ibuf, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.fhost.numpy(), self.ihost.numpy()
+
+    def run(self, pairs, seeds, q_iters: int, classify_tol: float):
+        self.set_pairs(pairs)
+        self.set_seeds(seeds)
+        self.launch(q_iters, classify_tol)
+        return self.fetch()
+
+
+_SMALL_PLANS: dict = {}
+
+
+def small_batch_plan(B: int, n: int, k: int) -> SmallBatchPlan:
+    key = (B, n, k)
+    if key not in _SMALL_PLANS:
+        _SMALL_PLANS[key] = SmallBatchPlan(B, n, k)
+    return _SMALL_PLANS[key]

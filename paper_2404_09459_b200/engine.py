@@ -355,9 +355,55 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
         return [_general_run(pr, dataclasses.replace(
             opts, extraction=dataclasses.replace(cfg, seed=sd))) for pr, sd in zip(pairs, seeds)]
     k1, k2 = widths
+    if _dev.small_batch_fits(max(first.m, first.p), first.n, k1, k2):
+        return _small_batch_runs(pairs, opts, seeds, k1)
     plan = _dev.batch_plan(len(pairs), first.m, first.p, first.n, k1, k2)
     pks = plan.run([(pr.g1, pr.g2) for pr in pairs], seeds, cfg.power_iters, opts.classify_tol)
     return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]
+
+
+def _small_batch_runs(pairs, opts: GsvOptions, seeds, k: int) -> list:
+    """Many small pairs through rgsv_batch_gsvd (one fused chain launch for
+    every matrix, one small-GSVD launch for every pair)."""
+    n = pairs[0].n
+    plan = _dev.small_batch_plan(len(pairs), n, k)
+    fh, ih = plan.run([(pr.g1, pr.g2) for pr in pairs], seeds, opts.extraction.power_iters,
+                      opts.classify_tol)
+    return unpack_small_batch(fh, ih, plan, opts)
+
+
+def unpack_small_batch(fh, ih, plan, opts: GsvOptions) -> list:
+    B, n, k, rs = plan.B, plan.n, plan.k, plan.res_stride
+    stats = fh[B * rs:].reshape(B, 4)
+    status_all = ih[4 * B:]
+    runs = []
+    for j in range(B):
+        o = fh[j * rs:(j + 1) * rs]
+        status = int(status_all[j])
+        bases = []
+        for gf2, energy in ((stats[j, 0], stats[j, 1]), (stats[j, 2], stats[j, 3])):
+            if not math.isfinite(gf2):
+                raise ValidationError("g contains non-finite entries")
+            hist = _dev.residual_history(float(gf2), float(energy))
+            tol = opts.extraction.tol if opts.extraction.tol is not None else 1e-10 * hist[0]
+            bases.append(BasisResult(None, hist, hist[-1] < tol, 1, [k]))
+        if status & ST_OMEGA_SHORT:
+            raise RuntimeError("device Omega generator exhausted its draw margin")
+        if status & ST_CHOL:
+            raise RankDeficiencyError(f"CholeskyQR breakdown in batch pair {j}")
+        if status & ST_JACOBI:
+            raise ConvergenceError("Jacobi SVD of an L block did not converge")
+        if status & ST_CLASSIFY:
+            raise ValidationError("overlapping zero classifications; sequences not ordered?")
+        nsv1, nsv2, r, s = (int(x) for x in ih[4 * j: 4 * j + 4])
+        spec = GsvSpectrum(o[:n].copy(), o[n:2 * n].copy(), r, s)
+        sc = o[6 * n: 6 * n + 4]
+        runs.append(DeviceRun(spec, spec.alphas, spec.betas, r, s, o[2 * n:3 * n].copy(),
+                              o[3 * n:4 * n].copy(), o[4 * n:5 * n].copy(), o[5 * n:6 * n].copy(),
+                              float(sc[0]), float(sc[1]), (float(sc[2]), float(sc[3])), status,
+                              bases[0], bases[1], o[6 * n + 4: 6 * n + 4 + nsv1].copy(),
+                              o[6 * n + 4 + k: 6 * n + 4 + k + nsv2].copy(), plan))
+    return runs
 
 
 def compute_gsv_batch(pairs, opts: GsvOptions | None = None, seeds=None) -> list:

@@ -1,0 +1,113 @@
+"""Batched small-pair path (rgsv_batch_gsvd, SURVEY.md §8 cfg3 shapes).
+
+Each pair of a batch must equal the single-pair device pipeline and the
+oracle's fixed-rank restatement on the same seeds: spectrum and counts
+exactly, residual energies to 1e-12, the leading s rows of B to 1e-12
+(parity contract), comparative quantities to 1e-12.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import rgsv_oracle as orc
+from paper_2404_09459_b200.workloads import CONFIGS, batch_seeds, make_pair
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rg():
+    import paper_2404_09459_b200 as rg
+
+    rg._native.require_device()
+    return rg
+
+
+def _pairs(rg, cfg, B, m=None, p=None):
+    hosts, pairs, seeds = [], [], []
+    for j in range(B):
+        ds, os_ = batch_seeds(j)
+        g1, g2 = make_pair(cfg, data_seed=ds, m=m, p=p)
+        hosts.append((g1, g2))
+        pairs.append(rg.GmpPair.resident(torch.from_numpy(g1).cuda(),
+                                         torch.from_numpy(g2).cuda()))
+        seeds.append(os_)
+    return hosts, pairs, seeds
+
+
+@pytest.mark.parametrize("B,m,p", [(6, None, None), (3, 1000, 517), (2, 9000, 77)])
+def test_batch_matches_single_and_oracle(rg, B, m, p):
+    cfg = CONFIGS["cfg3"]
+    hosts, pairs, seeds = _pairs(rg, cfg, B, m, p)
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(cfg.k, 0, cfg.q))
+    # 9000 rows exceed the clustered Y slice: the engine takes the per-pair
+    # stream plan instead, and the results must not depend on which
+    assert rg.device.small_batch_fits(max(hosts[0][0].shape[0], hosts[0][1].shape[0]), cfg.n,
+                                      cfg.k, cfg.k) == (m != 9000)
+    runs = rg.engine.run_device_batch(pairs, opts, seeds)
+    for j, (run, (g1, g2)) in enumerate(zip(runs, hosts)):
+        single = rg.engine.run_device_pipeline(
+            pairs[j], rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(cfg.k, seeds[j],
+                                                                               cfg.q)))
+        assert np.array_equal(run.alphas, single.alphas)
+        assert (run.r, run.s) == (single.r, single.s)
+        for a, b in ((run.theta, single.theta), (run.p1, single.p1), (run.p2, single.p2)):
+            assert np.max(np.abs(a - b)) <= 1e-12
+        o = orc.run_pipeline(g1, g2, k=cfg.k, q=cfg.q, seed=seeds[j])
+        assert np.array_equal(run.alphas, o.alphas) and (run.r, run.s) == (o.r, o.s)
+        for basis, ob in ((run.basis1, o.basis1), (run.basis2, o.basis2)):
+            h, ho = basis.residual_history, ob.residual_history
+            assert abs(h[0] - ho[0]) <= 1e-13 * ho[0]
+            e, eo = h[0] ** 2 - h[1] ** 2, ho[0] ** 2 - ho[1] ** 2
+            assert abs(e - eo) <= 1e-12 * eo
+
+
+def test_batch_projections_match_oracle_rows(rg):
+    cfg = CONFIGS["cfg3"]
+    B = 4
+    hosts, pairs, seeds = _pairs(rg, cfg, B)
+    plan = rg.device.small_batch_plan(B, cfg.n, cfg.k)
+    plan.set_pairs([(pr.g1, pr.g2) for pr in pairs])
+    plan.set_seeds(seeds)
+    kp, ldo = 16, 64
+    bo = torch.zeros((2 * B, kp, ldo), dtype=torch.float64, device="cuda")
+    plan.launch(cfg.q, 1e-10, b_out=bo)
+    plan.fetch()
+    b = bo.cpu().numpy()
+    s = cfg.s
+    for j, (g1, g2) in enumerate(hosts):
+        for i, (g, sd) in enumerate(((g1, seeds[j]), (g2, seeds[j] + 1))):
+            ob = orc.fixed_rank_basis(g, cfg.k, cfg.q, sd).b
+            lead = ob[:s]
+            assert np.linalg.norm(b[2 * j + i, :s, : cfg.n] - lead) <= 1e-12 * np.linalg.norm(lead)
+            # full k-row block: same span (rows are an orthonormal-basis image)
+            sv_d = np.linalg.svd(b[2 * j + i, : cfg.k, : cfg.n], compute_uv=False)
+            sv_o = np.linalg.svd(ob, compute_uv=False)
+            assert np.max(np.abs(sv_d[:s] - sv_o[:s])) <= 1e-12 * sv_o[0]
+            assert not np.any(b[2 * j + i, cfg.k:])
+
+
+def test_batch_full_cfg3_scale_invariants(rg):
+    """All 4096 cfg3 pairs in one call: size-independent properties (every
+    spectrum is the F2 closed form, energies below |G|^2, entropies fixed)."""
+    cfg = CONFIGS["cfg3"]
+    B = cfg.batch
+    rng = torch.Generator(device="cuda").manual_seed(0)
+    g1 = torch.randn((B, cfg.m, cfg.n), generator=rng, device="cuda", dtype=torch.float64)
+    g2 = torch.randn((B, cfg.p, cfg.n), generator=rng, device="cuda", dtype=torch.float64)
+    pairs = [rg.GmpPair.resident(g1[j], g2[j]) for j in range(B)]
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(cfg.k, 0, cfg.q))
+    runs = rg.engine.run_device_batch(pairs, opts, [2 * j for j in range(B)])
+    closed = np.r_[np.ones(cfg.k), np.zeros(cfg.n - cfg.k)]
+    for run in runs[:: 97]:
+        assert np.array_equal(run.alphas, closed) and (run.r, run.s) == (cfg.k, 0)
+        h = run.basis1.residual_history
+        assert 0.0 < h[1] < h[0]
+    # spot-check a few pairs against the single-pair pipeline
+    for j in (0, 1234, B - 1):
+        single = rg.engine.run_device_pipeline(
+            pairs[j], rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(cfg.k, 2 * j, cfg.q)))
+        e_b = runs[j].basis1.residual_history
+        e_s = single.basis1.residual_history
+        assert abs((e_b[0] ** 2 - e_b[1] ** 2) - (e_s[0] ** 2 - e_s[1] ** 2)) <= 1e-12 * e_s[0] ** 2
