@@ -108,6 +108,10 @@ typedef struct {
  * largest matrix fits shared memory in a cluster of <= 8 CTAs), else 0. */
 int rgsv_batch_supported(int max_rows, int64_t n, int k);
 size_t rgsv_batch_workspace_bytes(int npairs, int64_t n, int k);
+/* Diagnostic: per-phase clock64 totals of the batched chain kernel (16
+ * counters), only in a library built with -DRGSV_BATCH_PROFILE
+ * (tools/batch_phases.py); RGSV_ERR_VALIDATION otherwise. */
+int rgsv_debug_batch_profile(unsigned long long* out16, int reset);
 int rgsv_batch_gsvd(const void* mats, int npairs, int max_rows, int64_t n, int k, int q,
                     const uint64_t* seeds, double classify_tol, double* res, int* ints,
                     double* stats, int* status, double* b_out, void* workspace,

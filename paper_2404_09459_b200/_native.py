@@ -21,7 +21,7 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librgsv_b200.so")
+LIB_PATH = os.environ.get("RGSV_LIB_PATH") or os.path.join(HERE, "librgsv_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rgsv_b200.h")
 
 OK, ERR_DIMENSION, ERR_VALIDATION, ERR_RANK, ERR_CONVERGENCE, ERR_CUDA, ERR_WORKSPACE, \
@@ -53,6 +53,7 @@ SIGNATURES = {
                                 _p, _p, _p]),
     "rgsv_transpose": (_i32, [_p, _i64, _p, _i64, _i32, _i32, _p]),
     "rgsv_batch_supported": (_i32, [_i32, _i64, _i32]),
+    "rgsv_debug_batch_profile": (_i32, [_p, _i32]),
     "rgsv_batch_workspace_bytes": (_sz, [_i32, _i64, _i32]),
     "rgsv_batch_gsvd": (_i32, [_p, _i32, _i32, _i64, _i32, _i32, _p, _d, _p, _p, _p, _p, _p, _p,
                                _sz, _p]),

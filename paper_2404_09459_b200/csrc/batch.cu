@@ -22,6 +22,27 @@
 namespace rgsv {
 namespace {
 
+// Opt-in phase timers (compile with -DRGSV_BATCH_PROFILE; tools/batch_phases):
+// thread 0 of every CTA accumulates clock64 deltas per phase into
+// g_batch_prof[phase]. Off in the product build.
+#ifdef RGSV_BATCH_PROFILE
+}  // namespace
+__device__ unsigned long long g_batch_prof[16];
+namespace {
+#define PROF_T0() long long _pt = clock64()
+#define PROF(ph)                                                                  \
+  do {                                                                            \
+    if (threadIdx.x == 0) {                                                       \
+      long long _n = clock64();                                                   \
+      atomicAdd(&g_batch_prof[ph], (unsigned long long)(_n - _pt));               \
+      _pt = _n;                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define PROF_T0()
+#define PROF(ph)
+#endif
+
 constexpr int kTR = 32;       // G rows per streamed tile
 constexpr int kStages = 3;    // cp.async ring depth
 constexpr int kThreads = 256; // 8 warps
@@ -200,16 +221,28 @@ struct Chain {
   // ---- Y[t-tile] = G_tile X  (pass A); optional sum of squares of G
   RGSV_DI void pass_gx(const BatchMat& g, int r0, int r1, int n, double* ss) {
     constexpr int kRB = kTR / 8, kCB = KP / 8, kBlocks = kRB * kCB;
+    static_assert(kBlocks % kWarps == 0, "whole blocks per warp");
+    constexpr int kPer = kBlocks / kWarps;
+    // X fragments are the same for every tile: keep them in registers
+    double xf[kPer][NP / 4];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int cb = (warp + i * kWarps) / kRB;
+      const double* brow = xt + (cb * 8 + (lane >> 2)) * GP + (lane & 3);
+#pragma unroll
+      for (int ks = 0; ks < NP / 4; ++ks) xf[i][ks] = brow[ks * 4];
+    }
     stream_g(g, r0, r1, n, [&](int t, const double* gt) {
-      for (int b = warp; b < kBlocks; b += kWarps) {
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int b = warp + i * kWarps;
         const int rb = b % kRB, cb = b / kRB;
         double cc[4][2] = {};
         const double* arow = gt + (rb * 8 + (lane >> 2)) * GP + (lane & 3);
-        const double* brow = xt + (cb * 8 + (lane >> 2)) * GP + (lane & 3);
 #pragma unroll
         for (int ks = 0; ks < NP / 4; ks += 4) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dmma(cc[u], arow[(ks + u) * 4], brow[(ks + u) * 4]);
+          for (int u = 0; u < 4; ++u) dmma(cc[u], arow[(ks + u) * 4], xf[i][ks + u]);
         }
         double c[2] = {(cc[0][0] + cc[1][0]) + (cc[2][0] + cc[3][0]),
                        (cc[0][1] + cc[1][1]) + (cc[2][1] + cc[3][1])};
@@ -365,22 +398,16 @@ struct Chain {
         }
         bad |= !(d > 0.0) || !isfinite(d);
         const double r = rsqrt(d);
-        const double f = a[j] * (r * r);  // A[i][j] / d
-        if (lane > j) {
+        // branch-free row operation: rows below eliminate (ff = A[i][j] / d),
+        // the pivot row scales by d^-1/2 (mul = r), rows above are untouched
+        const double ff = (lane > j) ? a[j] * (r * r) : 0.0;
+        const double mul = (lane == j) ? r : 1.0;
 #pragma unroll
-          for (int c = 0; c < KP; ++c) {
-            if (c > j) a[c] = fma(-f, pa[c], a[c]);
-            if (c <= j) x[c] = fma(-f, px[c], x[c]);
-          }
-          a[j] = 0.0;
-        } else if (lane == j) {
-#pragma unroll
-          for (int c = 0; c < KP; ++c) {
-            if (c > j) a[c] *= r;
-            if (c <= j) x[c] *= r;
-          }
-          a[j] = d * r;
+        for (int c = 0; c < KP; ++c) {
+          if (c > j) a[c] = fma(-ff, pa[c], a[c]) * mul;
+          if (c <= j) x[c] = fma(-ff, px[c], x[c]) * mul;
         }
+        a[j] = (lane > j) ? 0.0 : (lane == j ? d * r : a[j]);
       }
       if (bad) fail = 1;
       if (lane < KP) {
@@ -396,21 +423,41 @@ struct Chain {
   RGSV_DI void trsm(double* buf, int rows) {
     constexpr int LD = KP + 1;
     const int nrb = (rows + 7) / 8;
-    for (int rb = warp; rb < nrb; rb += kWarps) {
-      const int r = rb * 8 + (lane >> 2);
-      double a[KP / 4];
+    // L^-T fragments are shared by every row block: registers
+    double lf[KP / 8][KP / 4];
 #pragma unroll
-      for (int ks = 0; ks < KP / 4; ++ks) a[ks] = buf[yx<KP>(r, ks * 4 + (lane & 3))];
-      __syncwarp();
+    for (int cb = 0; cb < KP / 8; ++cb)
 #pragma unroll
-      for (int cb = 0; cb < KP / 8; ++cb) {
-        double c[2] = {0.0, 0.0};
+      for (int ks = 0; ks < KP / 4; ++ks)
+        lf[cb][ks] = linv[(cb * 8 + (lane >> 2)) * LD + ks * 4 + (lane & 3)];
+    // two row blocks per iteration: independent DMMA chains
+    for (int rb0 = warp * 2; rb0 < nrb; rb0 += kWarps * 2) {
+      double a[2][KP / 4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = (rb0 + h) * 8 + (lane >> 2);
 #pragma unroll
         for (int ks = 0; ks < KP / 4; ++ks)
-          dmma(c, a[ks], linv[(cb * 8 + (lane >> 2)) * LD + ks * 4 + (lane & 3)]);
-        const int col = cb * 8 + 2 * (lane & 3);
-        buf[yx<KP>(r, col)] = c[0];
-        buf[yx<KP>(r, col + 1)] = c[1];
+          a[h][ks] = (rb0 + h < nrb) ? buf[yx<KP>(r, ks * 4 + (lane & 3))] : 0.0;
+      }
+      __syncwarp();
+      double c[2][KP / 8][2] = {};
+#pragma unroll
+      for (int ks = 0; ks < KP / 4; ++ks)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int cb = 0; cb < KP / 8; ++cb) dmma(c[h][cb], a[h][ks], lf[cb][ks]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (rb0 + h >= nrb) break;
+        const int r = (rb0 + h) * 8 + (lane >> 2);
+#pragma unroll
+        for (int cb = 0; cb < KP / 8; ++cb) {
+          const int col = cb * 8 + 2 * (lane & 3);
+          buf[yx<KP>(r, col)] = c[h][cb][0];
+          buf[yx<KP>(r, col + 1)] = c[h][cb][1];
+        }
       }
     }
     __syncthreads();
@@ -420,8 +467,10 @@ struct Chain {
   //      replicated small matrix (local Gram, no cluster traffic)
   RGSV_DI void cholqr3(double* buf, int rows, int k, int64_t shift_rows, bool sharded) {
     constexpr int LD = KP + 1;
+    PROF_T0();
     for (int pass = 0; pass < 3; ++pass) {
       gram_partial(buf, rows);
+      PROF(4);
       if (sharded) {
         reduce(KP * KP, [&](int e, double s) { gram[(e / KP) * LD + (e % KP)] = s; });
       } else {
@@ -430,8 +479,11 @@ struct Chain {
         for (int e = tid; e < KP * KP; e += kThreads) gram[(e / KP) * LD + (e % KP)] = src[e];
         __syncthreads();
       }
+      PROF(5);
       chol(k, pass == 0 ? shift_rows : 0);
+      PROF(6);
       trsm(buf, rows);
+      PROF(7);
     }
   }
 };
@@ -451,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
     const int rl = r1 - r0;
     const int rl32 = (rl + kTR - 1) / kTR * kTR;
     C.fail = 0;
+    PROF_T0();
     // X^T = Omega^T block (KP x n), zero-padded
     const double* om = A.omega + (int64_t)mat * A.om_stride;
     for (int e = C.tid; e < KP * NP; e += kThreads) {
@@ -461,8 +514,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
     __syncthreads();
     // (1) sketch Y = G Omega, ||G||^2 on the side
     double ss = 0.0;
+    PROF(0);
     C.pass_gx(g, r0, r1, n, &ss);
     __syncthreads();
+    PROF(1);
     // ||G||_F^2: block partial in fixed order -> cluster sum
     {
       double v = warp_sum(ss);
@@ -475,12 +530,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       }
       C.reduce(1, [&](int, double s) { C.misc[0] = s; });
     }
+    PROF(8);
     C.cholqr3(C.ys, rl32, k, rows, true);
+    PROF(9);
     for (int it = 0; it < A.q; ++it) {
       // (2) Z = G^T Q (n x k), cluster-reduced, then Qhat = cholqr3(Z)
       C.pass_gtq(g, r0, r1, n);
+      PROF(2);
       C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
+      PROF(10);
       C.cholqr3(C.zb, NP, k, n, false);
+      PROF(11);
       for (int e = C.tid; e < KP * NP; e += kThreads) {
         const int i = e / NP, j = e % NP;
         C.xt[i * C.GP + j] = (j < n) ? C.zb[yx<KP>(j, i)] : 0.0;
@@ -489,11 +549,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       // (3) Y = G Qhat, Q = cholqr3(Y)
       C.pass_gx(g, r0, r1, n, nullptr);
       __syncthreads();
+      PROF(1);
       C.cholqr3(C.ys, rl32, k, rows, true);
+      PROF(9);
     }
     // (4) B^T = G^T Q (n x k), cluster-reduced; rank 0 writes B and ||B||^2
     C.pass_gtq(g, r0, r1, n);
+    PROF(2);
     C.reduce(NP * KP, [&](int e, double s) { C.zb[e] = s; });
+    PROF(10);
     if (C.crank == 0) {
       double* bo = A.b_out + (int64_t)mat * A.b_stride;
       double e2 = 0.0;
@@ -518,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
     }
     (void)LD;
     __syncthreads();
+    PROF(12);
   }
   cluster_barrier();  // no CTA leaves while a peer may still read its slots
 }
@@ -606,3 +671,20 @@ int batch_chain(const BatchMat* mats, int nmat, int max_rows, int n, int k, int 
 }
 
 }  // namespace rgsv
+
+extern "C" int rgsv_debug_batch_profile(unsigned long long* out16, int reset) {
+#ifdef RGSV_BATCH_PROFILE
+  if (out16 && cudaMemcpyFromSymbol(out16, rgsv::g_batch_prof, sizeof(unsigned long long) * 16) !=
+                   cudaSuccess)
+    return RGSV_ERR_CUDA;
+  if (reset) {
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(rgsv::g_batch_prof, z, sizeof(z)) != cudaSuccess) return RGSV_ERR_CUDA;
+  }
+  return 0;
+#else
+  (void)out16;
+  (void)reset;
+  return RGSV_ERR_VALIDATION;  // library built without -DRGSV_BATCH_PROFILE
+#endif
+}
