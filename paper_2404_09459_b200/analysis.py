@@ -17,7 +17,15 @@ import torch
 
 from . import device as _dev
 from ._native import ST_DEGENERATE, ST_NOT_NORMALIZED, check, lib
-from .engine import GmpPair, GsvOptions, GsvSpectrum, run_device_batch, run_device_pipeline
+from .engine import (
+    GmpPair,
+    GsvOptions,
+    GsvSpectrum,
+    SmallBatchRuns,
+    _MappedSeq,
+    run_device_batch,
+    run_device_pipeline,
+)
 from .errors import DegenerateSpectrumError, ValidationError
 
 QUARTER_PI = math.pi / 4
@@ -113,7 +121,15 @@ def compare_batch(pairs, opts: GsvOptions | None = None, seeds=None) -> list:
     """compare over a batch of same-shape pairs run concurrently on the
     device (throughput mode); equal to per-pair compare calls."""
     opts = opts or GsvOptions()
-    return [_report(run, opts) for run in run_device_batch(pairs, opts, seeds)]
+    runs = run_device_batch(pairs, opts, seeds)
+    if isinstance(runs, SmallBatchRuns):
+        st = runs.status
+        if np.any(st & ST_DEGENERATE):
+            raise DegenerateSpectrumError("spectrum has vanishing alpha- or beta-energy")
+        if np.any(st & ST_NOT_NORMALIZED):
+            raise ValidationError("eigenexpression fractions do not sum to 1")
+        return _MappedSeq(runs, lambda run: _report(run, opts))
+    return [_report(run, opts) for run in runs]
 
 
 def compare(pair: GmpPair, opts: GsvOptions | None = None) -> ComparativeReport:

@@ -486,11 +486,11 @@ class SmallBatchPlan:
         self._seed_key = None
 
     def set_pairs(self, pairs) -> int:
-        """Descriptors {G1_j, G2_j} of the (resident) pairs; returns max rows."""
-        mats = []
-        for g1, g2 in pairs:
-            mats += [g1, g2]
-        key = tuple((g.t.data_ptr(), g.ld, g.rows) for g in mats)
+        """Descriptors {G1_j, G2_j} of the (resident) pairs; returns max rows.
+        Cached on the identity of the matrix objects (kept referenced here so
+        the identities stay valid while cached)."""
+        mats = [g for pair in pairs for g in pair]
+        key = tuple(map(id, mats))
         if key != self._desc_key:
             arr = np.zeros(len(mats), dtype=_DESC)
             arr["g"] = [g.t.data_ptr() for g in mats]
@@ -498,17 +498,18 @@ class SmallBatchPlan:
             arr["rows"] = [g.rows for g in mats]
             self.desc.copy_(torch.from_numpy(arr.view(np.uint8)))
             self._desc_key = key
-            self.max_rows = max(g.rows for g in mats)
+            self._desc_refs = mats
+            self.max_rows = int(arr["rows"].max())
         return self.max_rows
 
     def set_seeds(self, seeds) -> None:
-        key = tuple(seeds)
-        if key != self._seed_key:
-            words = []
-            for s in seeds:  # G1: seed, G2: seed + 1 (engine.py:252-253)
-                words += [seed_word(s), seed_word(int(s) + 1)]
-            self.seeds.copy_(torch.tensor(words, dtype=torch.int64))
-            self._seed_key = key
+        """Omega stream seeds: G1_j from seeds[j], G2_j from seeds[j] + 1
+        (engine.py:252-253), reduced mod 2^64 like rangefinder.py:101."""
+        sd = np.fromiter((int(x) & SEED_MASK for x in seeds), dtype=np.uint64, count=len(seeds))
+        words = np.empty(2 * len(sd), dtype=np.uint64)
+        words[0::2] = sd
+        words[1::2] = sd + np.uint64(1)  # wraps mod 2^64
+        self.seeds.copy_(torch.from_numpy(words.view(np.int64)))
 
     def launch(self, q_iters: int, classify_tol: float, stream=None, b_out=None) -> None:
         """b_out: optional (2B x kp x ceil16(n)) tensor receiving every B."""

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -362,55 +363,117 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
     return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]
 
 
-def _small_batch_runs(pairs, opts: GsvOptions, seeds, k: int) -> list:
+def _small_batch_runs(pairs, opts: GsvOptions, seeds, k: int):
     """Many small pairs through rgsv_batch_gsvd (one fused chain launch for
     every matrix, one small-GSVD launch for every pair)."""
     n = pairs[0].n
     plan = _dev.small_batch_plan(len(pairs), n, k)
     fh, ih = plan.run([(pr.g1, pr.g2) for pr in pairs], seeds, opts.extraction.power_iters,
                       opts.classify_tol)
-    return unpack_small_batch(fh, ih, plan, opts)
+    return SmallBatchRuns(fh, ih, plan, opts)
 
 
-def unpack_small_batch(fh, ih, plan, opts: GsvOptions) -> list:
-    B, n, k, rs = plan.B, plan.n, plan.k, plan.res_stride
-    stats = fh[B * rs:].reshape(B, 4)
-    status_all = ih[4 * B:]
-    runs = []
-    for j in range(B):
-        o = fh[j * rs:(j + 1) * rs]
-        status = int(status_all[j])
+def _trusted_spectrum(a, b, r: int, s: int) -> GsvSpectrum:
+    """GsvSpectrum whose invariants were already checked (vectorized)."""
+    spec = object.__new__(GsvSpectrum)
+    object.__setattr__(spec, "alphas", a)
+    object.__setattr__(spec, "betas", b)
+    object.__setattr__(spec, "r", r)
+    object.__setattr__(spec, "s", s)
+    return spec
+
+
+class SmallBatchRuns(Sequence):
+    """Results of one rgsv_batch_gsvd call, validated for the whole batch at
+    once (status bits, finiteness and every GsvSpectrum invariant of
+    engine.py:108-125, vectorized); per-pair DeviceRun objects are built on
+    access, so a 4096-pair step costs one D2H copy plus a few numpy passes."""
+
+    def __init__(self, fh, ih, plan, opts: GsvOptions):
+        B, n, k, rs = plan.B, plan.n, plan.k, plan.res_stride
+        self.B, self.n, self.k, self.plan, self.opts = B, n, k, plan, opts
+        self.res = fh[: B * rs].reshape(B, rs).copy()
+        self.stats = fh[B * rs: B * rs + 4 * B].reshape(B, 4).copy()
+        self.ints = ih[: 4 * B].reshape(B, 4).copy()
+        self.status = ih[4 * B: 5 * B].copy()
+        st = self.status
+        for bit, exc, msg in ((ST_OMEGA_SHORT, RuntimeError,
+                               "device Omega generator exhausted its draw margin"),
+                              (ST_CHOL, RankDeficiencyError, "CholeskyQR breakdown"),
+                              (ST_JACOBI, ConvergenceError, "Jacobi SVD did not converge"),
+                              (ST_CLASSIFY, ValidationError,
+                               "overlapping zero classifications; sequences not ordered?")):
+            bad = np.flatnonzero(st & bit)
+            if bad.size:
+                raise exc(f"{msg} (batch pair {int(bad[0])})")
+        if not np.all(np.isfinite(self.stats[:, 0])) or not np.all(np.isfinite(self.stats[:, 2])):
+            raise ValidationError("g contains non-finite entries")
+        a, b = self.res[:, :n], self.res[:, n:2 * n]
+        r, s = self.ints[:, 2], self.ints[:, 3]
+        if np.any(r < 0) or np.any(s < 0) or np.any(r + s > n):
+            raise ValidationError("invalid counts r, s")
+        if np.any(a < 0) or np.any(a > 1) or np.any(b < 0) or np.any(b > 1):
+            raise ValidationError("GSVs must lie in [0, 1]")
+        if np.any(np.diff(a, axis=1) > 1e-12) or np.any(np.diff(b, axis=1) < -1e-12):
+            raise ValidationError("alphas must be nonincreasing and betas nondecreasing")
+        if float(np.max(np.abs(a ** 2 + b ** 2 - 1.0))) > 1e-12:
+            raise ValidationError("alpha_i^2 + beta_i^2 = 1 violated beyond 1e-12")
+        idx = np.arange(n)
+        if np.any((b != 0.0) & (idx < r[:, None])) or np.any((a != 0.0) & (idx >= (r + s)[:, None])):
+            raise ValidationError("classified-zero entries must be exactly 0")
+
+    def __len__(self) -> int:
+        return self.B
+
+    def __getitem__(self, j):
+        if isinstance(j, slice):
+            return [self[i] for i in range(*j.indices(self.B))]
+        if j < 0:
+            j += self.B
+        if not 0 <= j < self.B:
+            raise IndexError(j)
+        n, k, o = self.n, self.k, self.res[j]
+        nsv1, nsv2, r, s = (int(x) for x in self.ints[j])
+        spec = _trusted_spectrum(o[:n].copy(), o[n:2 * n].copy(), r, s)
         bases = []
-        for gf2, energy in ((stats[j, 0], stats[j, 1]), (stats[j, 2], stats[j, 3])):
-            if not math.isfinite(gf2):
-                raise ValidationError("g contains non-finite entries")
+        for gf2, energy in ((self.stats[j, 0], self.stats[j, 1]),
+                            (self.stats[j, 2], self.stats[j, 3])):
             hist = _dev.residual_history(float(gf2), float(energy))
-            tol = opts.extraction.tol if opts.extraction.tol is not None else 1e-10 * hist[0]
+            tol = self.opts.extraction.tol if self.opts.extraction.tol is not None \
+                else 1e-10 * hist[0]
             bases.append(BasisResult(None, hist, hist[-1] < tol, 1, [k]))
-        if status & ST_OMEGA_SHORT:
-            raise RuntimeError("device Omega generator exhausted its draw margin")
-        if status & ST_CHOL:
-            raise RankDeficiencyError(f"CholeskyQR breakdown in batch pair {j}")
-        if status & ST_JACOBI:
-            raise ConvergenceError("Jacobi SVD of an L block did not converge")
-        if status & ST_CLASSIFY:
-            raise ValidationError("overlapping zero classifications; sequences not ordered?")
-        nsv1, nsv2, r, s = (int(x) for x in ih[4 * j: 4 * j + 4])
-        spec = GsvSpectrum(o[:n].copy(), o[n:2 * n].copy(), r, s)
         sc = o[6 * n: 6 * n + 4]
-        runs.append(DeviceRun(spec, spec.alphas, spec.betas, r, s, o[2 * n:3 * n].copy(),
-                              o[3 * n:4 * n].copy(), o[4 * n:5 * n].copy(), o[5 * n:6 * n].copy(),
-                              float(sc[0]), float(sc[1]), (float(sc[2]), float(sc[3])), status,
-                              bases[0], bases[1], o[6 * n + 4: 6 * n + 4 + nsv1].copy(),
-                              o[6 * n + 4 + k: 6 * n + 4 + k + nsv2].copy(), plan))
-    return runs
+        return DeviceRun(spec, spec.alphas, spec.betas, r, s, o[2 * n:3 * n].copy(),
+                         o[3 * n:4 * n].copy(), o[4 * n:5 * n].copy(), o[5 * n:6 * n].copy(),
+                         float(sc[0]), float(sc[1]), (float(sc[2]), float(sc[3])),
+                         int(self.status[j]), bases[0], bases[1],
+                         o[6 * n + 4: 6 * n + 4 + nsv1].copy(),
+                         o[6 * n + 4 + k: 6 * n + 4 + k + nsv2].copy(), self.plan)
+
+
+class _MappedSeq(Sequence):
+    """Lazy per-element view over a SmallBatchRuns."""
+
+    def __init__(self, runs, fn):
+        self._runs, self._fn = runs, fn
+
+    def __len__(self) -> int:
+        return len(self._runs)
+
+    def __getitem__(self, j):
+        if isinstance(j, slice):
+            return [self[i] for i in range(*j.indices(len(self)))]
+        return self._fn(self._runs[j])
 
 
 def compute_gsv_batch(pairs, opts: GsvOptions | None = None, seeds=None) -> list:
     """compute_gsv over a batch of same-shape pairs, run concurrently on the
     device (throughput mode); results equal per-pair compute_gsv calls."""
     opts = opts or GsvOptions()
-    return [run.spectrum for run in run_device_batch(pairs, opts, seeds)]
+    runs = run_device_batch(pairs, opts, seeds)
+    if isinstance(runs, SmallBatchRuns):
+        return _MappedSeq(runs, lambda run: run.spectrum)
+    return [run.spectrum for run in runs]
 
 
 def compute_gsv(pair: GmpPair, opts: GsvOptions | None = None) -> GsvSpectrum:
