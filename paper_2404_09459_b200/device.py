@@ -408,6 +408,77 @@ class BatchPlan:
         return [plan.pk for plan in self.plans]
 
 
+class HostStreamPlan:
+    """B pairs whose G1, G2 live in HOST memory (the end-to-end path): the
+    H2D copies of every pair run back to back on one copy stream, and pair
+    b's captured compute graph starts on its own stream as soon as pair b's
+    copy event fires, so compute overlaps the transfers of the pairs behind
+    it and the step is bounded by the PCIe link, not by copy + compute."""
+
+    def __init__(self, B: int, m: int, p: int, n: int, k1: int, k2: int):
+        self.B, self.m, self.p, self.n = B, m, p, n
+        self.plans = [PairPlan(m, p, n, k1, k2) for _ in range(B)]
+        self.streams = [torch.cuda.Stream() for _ in range(B)]
+        self.copy_stream = torch.cuda.Stream()
+        self.events = [torch.cuda.Event() for _ in range(B)]
+        w = _even(n)
+        self.bufs = []
+        for _ in range(B):
+            d1 = torch.zeros((m, w), dtype=F64, device="cuda")
+            d2 = torch.zeros((p, w), dtype=F64, device="cuda")
+            self.bufs.append((DevMatrix(d1[:, :n], m, n), DevMatrix(d2[:, :n], p, n)))
+
+    @staticmethod
+    def _host(a, rows, cols, name):
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))
+        if t.dim() != 2 or tuple(t.shape) != (rows, cols):
+            raise DimensionError(f"{name}: expected shape {(rows, cols)}, got {tuple(t.shape)}")
+        if t.is_complex():
+            raise ValidationError(f"{name}: complex matrices are not supported by the B200 path")
+        if t.dtype != F64:
+            t = t.to(F64)
+        if not t.is_contiguous():
+            t = t.contiguous()
+        if not t.is_pinned():
+            t = t.pin_memory()  # async H2D needs page-locked memory
+        return t
+
+    def run(self, host_pairs, seeds, q_iters: int, classify_tol: float):
+        cur = torch.cuda.current_stream()
+        self.copy_stream.wait_stream(cur)
+        staged = [(self._host(h1, self.m, self.n, "g1"), self._host(h2, self.p, self.n, "g2"))
+                  for h1, h2 in host_pairs]
+        with torch.cuda.stream(self.copy_stream):
+            for (h1, h2), (d1, d2), ev in zip(staged, self.bufs, self.events):
+                d1.t.copy_(h1, non_blocking=True)
+                d2.t.copy_(h2, non_blocking=True)
+                ev.record(self.copy_stream)
+        for plan, st, ev, (d1, d2), seed in zip(self.plans, self.streams, self.events, self.bufs,
+                                                 seeds):
+            st.wait_stream(cur)
+            st.wait_event(ev)
+            with torch.cuda.stream(st):
+                plan.run(d1, d2, seed, q_iters, classify_tol, sync=False)
+        for st in self.streams:
+            cur.wait_stream(st)
+        cur.synchronize()  # the pinned staging (if any) is released only after this
+        return [plan.pk for plan in self.plans]
+
+
+_HOST_PLANS: dict = {}
+
+
+def host_stream_plan(B: int, m: int, p: int, n: int, k1: int, k2: int) -> HostStreamPlan:
+    key = (torch.cuda.current_device(), B, m, p, n, k1, k2)
+    plan = _HOST_PLANS.get(key)
+    if plan is None:
+        if len(_HOST_PLANS) > 2:
+            _HOST_PLANS.clear()
+        plan = HostStreamPlan(B, m, p, n, k1, k2)
+        _HOST_PLANS[key] = plan
+    return plan
+
+
 _BATCH_PLANS: dict = {}
 
 

@@ -336,6 +336,41 @@ def unpack(pk, plan, opts: GsvOptions) -> DeviceRun:
                      pk.h("sv1")[: nsv[0]].copy(), pk.h("sv2")[: nsv[1]].copy(), plan)
 
 
+def _is_host_pair(pr) -> bool:
+    return not isinstance(pr, GmpPair)
+
+
+def run_host_batch(host_pairs, opts: GsvOptions, seeds=None) -> list:
+    """B pairs given as (g1, g2) HOST arrays (numpy or torch CPU tensors,
+    pinned for full speed): streamed to the device with every pair's
+    compute overlapping the transfers behind it (device.HostStreamPlan).
+    Finiteness is checked by the device sum-of-squares pass of each chain
+    (a NaN/Inf in G surfaces as a non-finite ||G||_F, ValidationError)."""
+    host_pairs = [tuple(pr) for pr in host_pairs]
+    if not host_pairs:
+        return []
+    shapes = {(tuple(a.shape), tuple(b.shape)) for a, b in host_pairs}
+    if len(shapes) != 1:
+        raise DimensionError("compare_batch needs pairs of one shape")
+    (m, n1), (p, n) = next(iter(shapes))
+    if n1 != n:
+        raise DimensionError(f"g1 has {n1} columns but g2 has {n}")
+    if m + p < n:
+        raise RankDeficiencyError(f"stacked pair has {m + p} rows < {n} columns")
+    cfg = opts.extraction
+    seeds = [cfg.seed] * len(host_pairs) if seeds is None else list(seeds)
+    if len(seeds) != len(host_pairs):
+        raise DimensionError("one seed per pair")
+    widths = _fixed_width(opts, m, p, n)
+    if widths is None:
+        pairs = [GmpPair(a, b) for a, b in host_pairs]
+        return run_device_batch(pairs, opts, seeds)
+    k1, k2 = widths
+    plan = _dev.host_stream_plan(len(host_pairs), m, p, n, k1, k2)
+    pks = plan.run(host_pairs, seeds, cfg.power_iters, opts.classify_tol)
+    return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]
+
+
 def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
     """B pairs of one shape, concurrently (device.BatchPlan). Pair b uses
     extraction seed seeds[b] (default: opts.extraction.seed for every pair,
@@ -343,6 +378,8 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
     pairs = list(pairs)
     if not pairs:
         return []
+    if _is_host_pair(pairs[0]):
+        return run_host_batch(pairs, opts, seeds)
     first = pairs[0]
     for pr in pairs[1:]:
         if (pr.m, pr.p, pr.n) != (first.m, first.p, first.n):
@@ -468,7 +505,9 @@ class _MappedSeq(Sequence):
 
 def compute_gsv_batch(pairs, opts: GsvOptions | None = None, seeds=None) -> list:
     """compute_gsv over a batch of same-shape pairs, run concurrently on the
-    device (throughput mode); results equal per-pair compute_gsv calls."""
+    device (throughput mode); results equal per-pair compute_gsv calls.
+    Pairs are GmpPair objects (resident in HBM) or (g1, g2) host arrays,
+    which are streamed in with transfer/compute overlap."""
     opts = opts or GsvOptions()
     runs = run_device_batch(pairs, opts, seeds)
     if isinstance(runs, SmallBatchRuns):

@@ -111,3 +111,29 @@ def test_batch_full_cfg3_scale_invariants(rg):
         e_b = runs[j].basis1.residual_history
         e_s = single.basis1.residual_history
         assert abs((e_b[0] ** 2 - e_b[1] ** 2) - (e_s[0] ** 2 - e_s[1] ** 2)) <= 1e-12 * e_s[0] ** 2
+
+
+def test_host_stream_batch_equals_resident(rg):
+    """compare_batch on host (g1, g2) arrays (streamed, copy/compute overlap)
+    returns exactly what the resident-pair batch returns."""
+    cfg = CONFIGS["cfg0"]
+    hosts = [make_pair(cfg, data_seed=40 + j) for j in range(3)]
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(cfg.k, 0, cfg.q))
+    seeds = [5, 6, 7]
+    res_dev = rg.compare_batch([rg.GmpPair.resident(torch.from_numpy(a).cuda(),
+                                                    torch.from_numpy(b).cuda())
+                                for a, b in hosts], opts, seeds)
+    pinned = [(torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory())
+              for a, b in hosts]
+    for _ in range(3):  # eager, capture, replay
+        res_host = rg.compare_batch(pinned, opts, seeds)
+        for x, y in zip(res_dev, res_host):
+            assert np.array_equal(x.spectrum.alphas, y.spectrum.alphas)
+            assert np.array_equal(x.theta, y.theta) and x.d1 == y.d1 and x.d2 == y.d2
+    # numpy (pageable) inputs work too
+    res_np = rg.compare_batch(hosts, opts, seeds)
+    assert np.array_equal(res_np[2].p1, res_dev[2].p1)
+    bad = [(hosts[0][0].copy(), hosts[0][1])]
+    bad[0][0][3, 4] = np.nan
+    with pytest.raises(rg.ValidationError):
+        rg.compare_batch(bad, opts, [0])
