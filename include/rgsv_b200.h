@@ -136,6 +136,12 @@ int rgsv_svd_vectors(double* v, int64_t ldv, int nv, int len, double* acc, int64
 /* dst (cols x rows) = src^T, src rows x cols. */
 int rgsv_transpose(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
                    void* stream);
+/* dst (rows x cols, fp64) = src (fp32), exact promotion of a row block --
+ * the reference promotes fp32 input to fp64 (core.py:51-54); the cfg4
+ * pipeline streams fp32 G through this in row chunks instead of holding a
+ * 118 GB fp64 copy. */
+int rgsv_convert_f32(const float* src, int64_t lds, int64_t rows, int64_t cols, double* dst,
+                     int64_t ldd, void* stream);
 /* a[:, j] /= d[j] for j < cols (engine.py:335,357). */
 int rgsv_scale_cols(double* a, int64_t lda, int rows, int cols, const double* d, void* stream);
 

@@ -58,6 +58,7 @@ SIGNATURES = {
     "rgsv_batch_gsvd": (_i32, [_p, _i32, _i32, _i64, _i32, _i32, _p, _d, _p, _p, _p, _p, _p, _p,
                                _sz, _p]),
     "rgsv_scale_cols": (_i32, [_p, _i64, _i32, _i32, _p, _p]),
+    "rgsv_convert_f32": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p]),
     "rgsv_sketch_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "rgsv_sketch_project": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _i32, _i32, _p, _p, _i64, _p,
                                    _p, _p, _p, _sz, _p]),

@@ -31,6 +31,8 @@ int launch_jacobi_vec(double* v, int64_t ldv, int nv, int len, double* acc, int6
                       int* nzero, int* status, cudaStream_t st);
 int launch_scale_cols(double* a, int64_t lda, int rows, int cols, const double* d,
                       cudaStream_t st);
+int launch_convert_f32(const float* src, int64_t lds, int64_t rows, int64_t cols, double* dst,
+                       int64_t ldd, cudaStream_t st);
 int launch_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
                 double alpha, cudaStream_t st);
 int debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
@@ -195,6 +197,12 @@ int rgsv_transpose(double* dst, int64_t ldd, const double* src, int64_t lds, int
   if (rows < 0 || cols < 0 || ldd < rows || lds < cols) return RGSV_ERR_DIMENSION;
   return launch_copy_block(dst, ldd, src, lds, cols, rows, 1,
                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_convert_f32(const float* src, int64_t lds, int64_t rows, int64_t cols, double* dst,
+                     int64_t ldd, void* stream) {
+  if (rows < 0 || cols < 0 || lds < cols || ldd < cols) return RGSV_ERR_DIMENSION;
+  return launch_convert_f32(src, lds, rows, cols, dst, ldd, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rgsv_scale_cols(double* a, int64_t lda, int rows, int cols, const double* d, void* stream) {
@@ -399,7 +407,9 @@ SmallLayout small_layout(int l1, int l2, int64_t n) {
   L.lds = ceil16(n);
   L.kpn = ceil16(n);
   const int64_t rows = L.lp > l ? L.lp : l;
-  const int64_t kmax = L.lp > L.kpn ? L.lp : L.kpn;
+  // factor size: the wide branch (l <= n) factors lp x lp Grams, the tall
+  // branch (l > n) kpn x kpn ones -- never max of both (cfg4: n = 8192, l = 576)
+  const int64_t kmax = (l > n) ? L.kpn : L.lp;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -466,7 +476,7 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
     // S = [B1; B2] (l x n, wide). S^T = P T (CholQR3 on S^T), so
     // range(S) = range(T^T) and the Q of qr(S) is the Q of qr(T^T).
     if (int e = launch_stack(S, lds, b1, ldb1, l1, b2, ldb2, l2, (int)lp, n, st)) return e;
-    if (lp > 512) return RGSV_ERR_DIMENSION;
+    if (lp > 1024) return RGSV_ERR_DIMENSION;
     double* pt = nullptr;
     if (int e = cholqr3_wide(S, S2, n, lds, l, (int)lp, gram, linv, rinv, rdiag, scratch, sb,
                              status, &pt, st))

@@ -48,10 +48,11 @@ __global__ void __launch_bounds__(512) k_chol_inv(const double* __restrict__ gra
     }
   }
   __syncthreads();
-  // kp is a multiple of 16 <= 512: thread -> (column c, row phase)
-  const int cpt = kp;                  // columns covered per row pass
+  // thread -> (column c, row phase); kp > nt (stacked pairs of cfg4, kp up
+  // to 1024): each thread owns the columns tid, tid + nt, ...
+  const int cpt = kp < nt ? kp : nt;   // columns covered per row pass
   const int rstep = nt / cpt > 0 ? nt / cpt : 1;
-  const int c = tid % cpt, r0 = tid / cpt;
+  const int c0 = tid % cpt, r0 = tid / cpt;
   for (int j = 0; j < k; ++j) {
     const double d = W[j * ldw + j];
     if (!(d > 0.0) || !isfinite(d)) {
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(512) k_chol_inv(const double* __restrict__ gra
       break;
     }
     const double inv_d = 1.0 / d;
-    if (c < k && r0 < rstep) {
+    for (int c = c0; c < k && r0 < rstep; c += cpt) {
       const double xjc = (c < j) ? W[c * ldw + j] : 1.0;  // X[j][c], X[j][j] = 1
       const double wcj = (c > j) ? W[c * ldw + j] : 0.0;   // column j entry of row c
       for (int i = j + 1 + r0; i < k; i += rstep) {
@@ -518,7 +519,7 @@ int chol_profile(const double* gram, int k, int kp, double* linv, long long* pro
 
 int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
              double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st) {
-  if (k <= 0 || kp < k || kp % 16 != 0 || kp > 512) return RGSV_ERR_DIMENSION;
+  if (k <= 0 || kp < k || kp % 16 != 0 || kp > 1024) return RGSV_ERR_DIMENSION;
   if (kp <= 128) {
     const size_t bytes = ((size_t)kp * (kp + 4) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
     static bool attr_blk = false;

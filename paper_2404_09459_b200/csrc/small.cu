@@ -258,6 +258,40 @@ int launch_jacobi_vec(double* v, int64_t ldv, int nv, int len, double* acc, int6
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
+// fp32 -> fp64 promotion of a row block (exact; the reference promotes fp32
+// input to fp64 at GmpPair construction, core.py:51-54). Row-major, 16-byte
+// vector loads when the pitches allow, zero padding up to the even pitch.
+__global__ void k_convert_f32(const float* __restrict__ src, int64_t lds, int64_t rows,
+                              int64_t cols, double* __restrict__ dst, int64_t ldd) {
+  const int64_t c4 = (cols + 3) / 4;
+  const int64_t total = rows * c4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / c4, c = (e % c4) * 4;
+    const float* s = src + r * lds + c;
+    double* d = dst + r * ldd + c;
+    if (c + 4 <= cols && ((reinterpret_cast<uintptr_t>(s) & 15) == 0) &&
+        ((reinterpret_cast<uintptr_t>(d) & 15) == 0)) {
+      const float4 v = *reinterpret_cast<const float4*>(s);
+      reinterpret_cast<double2*>(d)[0] = make_double2(v.x, v.y);
+      reinterpret_cast<double2*>(d)[1] = make_double2(v.z, v.w);
+    } else {
+      for (int64_t q = 0; q < 4 && c + q < cols; ++q) d[q] = (double)s[q];
+    }
+  }
+}
+
+int launch_convert_f32(const float* src, int64_t lds, int64_t rows, int64_t cols, double* dst,
+                       int64_t ldd, cudaStream_t st) {
+  const int64_t total = rows * ((cols + 3) / 4);
+  if (total <= 0) return 0;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 16 * kSMs) blocks = 16 * kSMs;
+  k_convert_f32<<<(int)blocks, 256, 0, st>>>(src, lds, rows, cols, dst, ldd);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
 // a (rows x cols) column j scaled by 1/d[j] (recover_gsvd, engine.py:335,357)
 __global__ void k_scale_cols(double* __restrict__ a, int64_t lda, int rows, int cols,
                              const double* __restrict__ d) {

@@ -55,18 +55,35 @@ class DevMatrix:
     def ld(self) -> int:
         return self.t.stride(0)
 
+    @property
+    def is_f32(self) -> bool:
+        return self.t.dtype == torch.float32
+
 
 def _even(x: int) -> int:
     return x + (x & 1)
 
 
-def to_device(a, name: str = "matrix") -> DevMatrix:
+def to_device(a, name: str = "matrix", keep_f32: bool = False) -> DevMatrix:
     """Validate shape/field like core.as_matrix (core.py:43-57) and place
     the matrix in HBM (no copy when it already is a suitable CUDA tensor).
-    Finiteness is checked on the device by the fused sum-of-squares pass."""
+    Finiteness is checked on the device by the fused sum-of-squares pass.
+    keep_f32: float32 input stays float32 in HBM (the cfg4 path promotes it
+    to fp64 chunk by chunk, exactly like the reference's up-front
+    promotion, core.py:51-54, but without a second full-size copy)."""
     require_device()
     if isinstance(a, DevMatrix):
         return a
+    is32 = (isinstance(a, torch.Tensor) and a.dtype == torch.float32) or \
+        (not isinstance(a, torch.Tensor) and np.asarray(a).dtype == np.float32)
+    if keep_f32 and is32:
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        if t.dim() != 2 or t.shape[0] < 1 or t.shape[1] < 1:
+            raise DimensionError(f"{name} must be 2-D with positive dimensions, got "
+                                 f"{tuple(t.shape)}")
+        if t.device.type != "cuda" or t.stride(1) != 1:
+            t = t.to("cuda").contiguous()
+        return DevMatrix(t, t.shape[0], t.shape[1])
     if isinstance(a, torch.Tensor):
         t = a
         if t.dim() != 2:
@@ -512,8 +529,31 @@ def residual_history(gf2: float, energy: float) -> list:
     return [math.sqrt(gf2), math.sqrt(max(gf2 - energy, 0.0))]
 
 
+STAGE_BYTES = 2 << 30  # fp64 staging for streamed fp32 row chunks
+
+
+def f64_chunks(g: DevMatrix, rows: int | None = None):
+    """Yield (r0, r1, DevMatrix) fp64 row blocks of g: views for fp64 input,
+    rgsv_convert_f32 promotions into one reused staging buffer for fp32."""
+    if not g.is_f32:
+        yield 0, g.rows, g
+        return
+    w = _even(g.cols)
+    R = rows or max(64, min(g.rows, STAGE_BYTES // (8 * w)))
+    stage = torch.zeros((min(R, g.rows), w), dtype=F64, device="cuda")
+    st = sp(torch.cuda.current_stream())
+    for r0 in range(0, g.rows, R):
+        r1 = min(g.rows, r0 + R)
+        check(lib().rgsv_convert_f32(ctypes.c_void_p(g.t.data_ptr() + r0 * g.ld * 4), g.ld,
+                                     r1 - r0, g.cols, vp(stage), w, st), "rgsv_convert_f32")
+        yield r0, r1, DevMatrix(stage[: r1 - r0, : g.cols], r1 - r0, g.cols)
+
+
 def device_sumsq(g: DevMatrix) -> float:
-    """||G||_F^2 on the device (core.sum_sq, core.py:115-125)."""
+    """||G||_F^2 on the device (core.sum_sq, core.py:115-125); fp32 input is
+    promoted chunk by chunk (squares of fp32 values are exact in fp64)."""
+    if g.is_f32:
+        return math.fsum(device_sumsq(c) for _, _, c in f64_chunks(g))
     out = torch.zeros(1, dtype=F64, device="cuda")
     ws = torch.empty(1024, dtype=F64, device="cuda")
     rc = lib().rgsv_sumsq(vp(g.t), g.ld, g.rows, g.cols, vp(out), vp(ws), ws.numel() * 8,

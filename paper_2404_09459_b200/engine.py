@@ -29,6 +29,7 @@ from .rangefinder import (
     BasisResult,
     ExtractionConfig,
     adaptive_device,
+    chunked_chain,
     check_max_cols,
     single_block_width,
 )
@@ -55,8 +56,8 @@ class GmpPair:
     check_rank: bool | None = None
 
     def __post_init__(self):
-        a = _dev.to_device(self.g1, "g1")
-        b = _dev.to_device(self.g2, "g2")
+        a = _dev.to_device(self.g1, "g1", keep_f32=True)
+        b = _dev.to_device(self.g2, "g2", keep_f32=True)
         if a.cols != b.cols:
             raise DimensionError(f"g1 has {a.cols} columns but g2 has {b.cols}")
         n = a.cols
@@ -86,8 +87,8 @@ class GmpPair:
         """Wrap device matrices without the validation passes (the bench
         path: G already resident in HBM, validated once at creation)."""
         pair = object.__new__(cls)
-        object.__setattr__(pair, "g1", _dev.to_device(g1, "g1"))
-        object.__setattr__(pair, "g2", _dev.to_device(g2, "g2"))
+        object.__setattr__(pair, "g1", _dev.to_device(g1, "g1", keep_f32=True))
+        object.__setattr__(pair, "g2", _dev.to_device(g2, "g2", keep_f32=True))
         object.__setattr__(pair, "check_rank", False)
         return pair
 
@@ -292,12 +293,46 @@ def _general_run(pair: GmpPair, opts: GsvOptions) -> DeviceRun:
                      bases[0], bases[1], out["sv1"], out["sv2"], None)
 
 
+def _promoted(pair: GmpPair) -> GmpPair:
+    """fp64 copy of an fp32 pair (core.py:51-54) for the small-size modes."""
+    p64 = object.__new__(GmpPair)
+    for name in ("g1", "g2"):
+        g = getattr(pair, name)
+        t = g.t.double() if g.is_f32 else g.t
+        object.__setattr__(p64, name, _dev.to_device(t, name))
+    object.__setattr__(p64, "check_rank", False)
+    return p64
+
+
+def _streamed_run(pair: GmpPair, opts: GsvOptions, k1: int, k2: int) -> DeviceRun:
+    """Fixed-rank pipeline for fp32-resident pairs (cfg4): both chains stream
+    G in fp64-promoted row chunks (rangefinder.chunked_chain), then the
+    shared small-GSVD + comparative stage."""
+    cfg = opts.extraction
+    _, b1, h1 = chunked_chain(pair.g1, k1, cfg.power_iters, cfg.seed)
+    _, b2, h2 = chunked_chain(pair.g2, k2, cfg.power_iters, cfg.seed + 1)
+    out = _small_checked(b1, k1, b2, k2, pair.n, opts.classify_tol)
+    r, s = out["counts"]
+    spec = GsvSpectrum(out["alphas"], out["betas"], r, s)
+    sc = out["scalars"]
+    bases = []
+    for h, k in ((h1, k1), (h2, k2)):
+        tol = cfg.tol if cfg.tol is not None else 1e-10 * h[0]
+        bases.append(BasisResult(None, h, h[-1] < tol, 1, [k]))
+    return DeviceRun(spec, spec.alphas, spec.betas, r, s, out["rho"], out["theta"], out["p1"],
+                     out["p2"], float(sc[0]), float(sc[1]), (float(sc[2]), float(sc[3])),
+                     out["status"], bases[0], bases[1], out["sv1"], out["sv2"], None)
+
+
 def run_device_pipeline(pair: GmpPair, opts: GsvOptions, *, sync: bool = True) -> DeviceRun:
     """The randomized path of _run_pipeline + spectrum_from_l_blocks +
     analysis, on the device (engine.py:245-275, analysis.py:82-102)."""
     widths = _fixed_width(opts, pair.m, pair.p, pair.n)
+    f32 = pair.g1.is_f32 or pair.g2.is_f32
     if widths is None:
-        return _general_run(pair, opts)
+        return _general_run(_promoted(pair) if f32 else pair, opts)
+    if f32:
+        return _streamed_run(pair, opts, *widths)
     k1, k2 = widths
     plan = _dev.pair_plan(pair.m, pair.p, pair.n, k1, k2)
     cfg = opts.extraction
@@ -381,6 +416,11 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
     if _is_host_pair(pairs[0]):
         return run_host_batch(pairs, opts, seeds)
     first = pairs[0]
+    if any(pr.g1.is_f32 or pr.g2.is_f32 for pr in pairs):  # streamed fp32 pairs, one by one
+        cfg0 = opts.extraction
+        seeds = [cfg0.seed] * len(pairs) if seeds is None else list(seeds)
+        return [run_device_pipeline(pr, dataclasses.replace(
+            opts, extraction=dataclasses.replace(cfg0, seed=sd))) for pr, sd in zip(pairs, seeds)]
     for pr in pairs[1:]:
         if (pr.m, pr.p, pr.n) != (first.m, first.p, first.n):
             raise DimensionError("compute_gsv_batch needs pairs of one shape")
@@ -533,6 +573,8 @@ def recover_gsvd(pair: GmpPair, opts: GsvOptions | None = None) -> GsvdFactors:
     if opts.method != DIRECT:
         check_max_cols(opts.extraction, pair.m, pair.n)
         check_max_cols(opts.extraction, pair.p, pair.n)
+    if pair.g1.is_f32 or pair.g2.is_f32:
+        pair = _promoted(pair)
     u, v, rf, spec = recover(pair, opts, opts.method == DIRECT)
     return GsvdFactors(u, v, rf, spec)
 

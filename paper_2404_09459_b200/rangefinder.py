@@ -286,6 +286,62 @@ def adaptive_device(a: "_dev.DevMatrix", cfg: ExtractionConfig):
     return qb[:, :lq], bb[:lq], BasisResult(None, history, converged, iterations, widths)
 
 
+def chunked_chain(a: "_dev.DevMatrix", k: int, q: int, seed: int, chunk_rows: int | None = None):
+    """The fixed-rank chain (sketch, shifted CholeskyQR3, q power iterations,
+    projection: rangefinder.py:115-123 + SURVEY.md §8(c)) with G streamed in
+    fp64 row chunks -- fp32 input is promoted chunk by chunk (the reference
+    promotes up front, core.py:51-54). Every GEMM pass converts each chunk
+    once and runs the DMMA GEMM on it; the Q^T G partials of the chunks are
+    summed in chunk order. Returns (Q: m x kp, B = Q^T G: kp x ldn, residual
+    history)."""
+    ops = _Ops()
+    m, n = a.rows, a.cols
+    if k > min(m, n):
+        raise ValidationError(f"max_cols={k} exceeds min(rows, cols)={min(m, n)}")
+    kp, ldn = _dev.ceil16(k), _dev.ceil16(n)
+    f64 = torch.float64
+    om = _dev.omega_device(n, k, [seed], ldo=ldn)[0]
+    ops.status.zero_()
+
+    def chunks():
+        return _dev.f64_chunks(a, chunk_rows)
+
+    def pass_gx(xt):
+        y = torch.zeros((m, kp), dtype=f64, device="cuda")
+        ss = []
+        for r0, r1, c in chunks():
+            ops.gx(_dev.vp(c.t), c.ld, _dev.vp(xt), ldn, _dev.vp(y[r0:]), kp, r1 - r0, kp, n)
+            if xt is om:
+                ss.append(ops.sumsq(_dev.vp(c.t), c.ld, r1 - r0, n))
+        return y, ss
+
+    def pass_gtq(qm):
+        acc = torch.zeros((kp, ldn), dtype=f64, device="cuda")
+        part = torch.zeros((kp, ldn), dtype=f64, device="cuda") if a.is_f32 else acc
+        for r0, r1, c in chunks():
+            ops.gtq(_dev.vp(qm[r0:]), kp, _dev.vp(c.t), c.ld, _dev.vp(part), ldn, kp, n, r1 - r0)
+            if part is not acc:
+                check(ops.L.rgsv_axpy(_dev.vp(acc), ldn, _dev.vp(part), ldn, kp, ldn, 1.0,
+                                      ops.st()), "axpy")
+        return acc
+
+    y, ss = pass_gx(om)
+    gf2 = math.fsum(ss)
+    if not math.isfinite(gf2):
+        raise ValidationError("g contains non-finite entries")
+    qm = ops.cholqr3(y, m, k, kp)
+    for _ in range(q):
+        zt = pass_gtq(qm)
+        qht = ops.wide_cholqr3(zt, n, ldn, k, kp)
+        y, _ = pass_gx(qht)
+        qm = ops.cholqr3(y, m, k, kp)
+    b = pass_gtq(qm)
+    energy = ops.sumsq(_dev.vp(b), ldn, k, n)
+    if int(ops.status.item()) & ST_CHOL:
+        raise RankDeficiencyError("CholeskyQR breakdown in the range finder (rank-deficient sketch)")
+    return qm, b, _dev.residual_history(gf2, energy)
+
+
 def extract_basis(g, cfg: ExtractionConfig | None = None, *, device_result: bool = False):
     """Extract an approximate orthonormal basis of range(g) on the B200
     (rangefinder.py:68-135). Returns the reference's ``BasisResult``; with
