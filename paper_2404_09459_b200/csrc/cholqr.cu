@@ -63,7 +63,29 @@ __global__ void __launch_bounds__(512) k_chol_inv(const double* __restrict__ gra
     for (int c = c0; c < k && r0 < rstep; c += cpt) {
       const double xjc = (c < j) ? W[c * ldw + j] : 1.0;  // X[j][c], X[j][j] = 1
       const double wcj = (c > j) ? W[c * ldw + j] : 0.0;   // column j entry of row c
-      for (int i = j + 1 + r0; i < k; i += rstep) {
+      int i = j + 1 + r0;
+      // Column j (rows > j) is read-only during step j and every target
+      // below is outside it, so batches of 8 loads can be in flight at once
+      // (matters for the global-memory variant: kp > 200 KB of shared).
+      for (; i + 7 * rstep < k; i += 8 * rstep) {
+        double lv[8], tv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) lv[u] = W[(i + u * rstep) * ldw + j] * inv_d;
+        if (c <= j) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) tv[u] = W[c * ldw + i + u * rstep];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) W[c * ldw + i + u * rstep] = tv[u] - lv[u] * xjc;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            tv[u] = (c <= i + u * rstep) ? W[(i + u * rstep) * ldw + c] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c <= i + u * rstep) W[(i + u * rstep) * ldw + c] = tv[u] - lv[u] * wcj;
+        }
+      }
+      for (; i < k; i += rstep) {
         const double lij = W[i * ldw + j] * inv_d;  // unit-lower L[i][j]
         if (c <= j) {
           W[c * ldw + i] -= lij * xjc;  // X[i][c] -= L[i][j] X[j][c]
