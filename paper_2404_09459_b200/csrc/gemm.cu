@@ -18,6 +18,8 @@
 // Work decomposition: blockIdx.x enumerates `full` whole-K tiles first, then
 // the tail tiles split `split` ways along K; split units write partials that
 // k_reduce_splits sums in a fixed order (results are bitwise deterministic).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "rgsv_internal.h"
 
@@ -49,8 +51,8 @@ RGSV_DI void decode_unit(const Decomp& d, int u, int& tile, int& c0, int& c1, in
 }
 
 // ------------------------------------------------------------------- gx
-template <int MT, int NT, int WM, int WN, int STAGES, bool SUMSQ>
-__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+template <int MT, int NT, int WM, int WN, int STAGES, bool SUMSQ, int MINB = 1>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     k_gx(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX,
          double* __restrict__ out, int64_t ld_out, double* __restrict__ part,
          int64_t part_stride, int part_row0, int M, int N, Decomp d,
@@ -173,8 +175,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 }
 
 // ------------------------------------------------------------------ gtq
-template <int MT, int NT, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+template <int MT, int NT, int WM, int WN, int STAGES, int MINB = 1>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     k_gtq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmG,
           double* __restrict__ out, int64_t ld_out, double* __restrict__ part,
           int64_t part_stride, int Mk, int N, Decomp d) {
@@ -332,13 +334,17 @@ int set_smem(K kernel, size_t bytes) {
   return 0;
 }
 
+// (2 CTAs/SM with a 4-stage ring was measured slower on the cfg1 shapes:
+// gtq 109 vs 99 us, gx 149 vs 90 us -- tools/gemm_ab.py; MINB stays a
+// template knob.)
 // Plan the unit list for `tiles` output tiles over `nchunks` K chunks.
-Decomp plan_units(int tiles_m, int tiles_n, int nchunks, int max_split, int* units, int* S) {
+Decomp plan_units(int tiles_m, int tiles_n, int nchunks, int max_split, int* units, int* S,
+                  int per_sm = 1) {
   Decomp d{};
   const int tiles = tiles_m * tiles_n;
   d.tiles_n = tiles_n;
   d.nchunks = nchunks;
-  const int slots = kSMs;
+  const int slots = kSMs * per_sm;
   // whole-K tiles fill complete waves; the remainder (rounded out to whole
   // tile rows so split rows never overlap whole-K rows) is split along K.
   const int waves = tiles / slots;
@@ -367,7 +373,7 @@ Decomp plan_units(int tiles_m, int tiles_n, int nchunks, int max_split, int* uni
   return d;
 }
 
-template <int MT, int NT, int WM, int WN, int STAGES, bool SUMSQ>
+template <int MT, int NT, int WM, int WN, int STAGES, bool SUMSQ, int MINB = 1>
 int run_gx(const GemmArgs& a, cudaStream_t st) {
   constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN;
   CUtensorMap tmG, tmX;
@@ -376,7 +382,7 @@ int run_gx(const GemmArgs& a, cudaStream_t st) {
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int nchunks = (int)((a.K + 15) / 16);
   int units, S;
-  Decomp d = plan_units(tiles_m, tiles_n, nchunks, a.max_split, &units, &S);
+  Decomp d = plan_units(tiles_m, tiles_n, nchunks, a.max_split, &units, &S, MINB);
   if (SUMSQ && tiles_n != 1) return RGSV_ERR_DIMENSION;
   int part_row0 = 0;
   if (S > 0) {
@@ -386,7 +392,7 @@ int run_gx(const GemmArgs& a, cudaStream_t st) {
   }
   const int64_t part_stride = (int64_t)(a.M - part_row0) * a.ldc;
   const size_t smem = STAGES * (BM + BN) * 128 + 2 * STAGES * 8 + 1024;
-  auto kern = k_gx<MT, NT, WM, WN, STAGES, SUMSQ>;
+  auto kern = k_gx<MT, NT, WM, WN, STAGES, SUMSQ, MINB>;
   if (int e = set_smem(kern, smem)) return e;
   kern<<<units, (WM * WN + 1) * 32, smem, st>>>(tmG, tmX, a.C, a.ldc, a.scratch, part_stride,
                                                  part_row0, (int)a.M, (int)a.N, d, a.ss_out);
@@ -402,7 +408,7 @@ int run_gx(const GemmArgs& a, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
-template <int MT, int NT, int WM, int WN, int STAGES>
+template <int MT, int NT, int WM, int WN, int STAGES, int MINB = 1>
 int run_gtq(const GemmArgs& a, cudaStream_t st) {
   constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN;
   CUtensorMap tmQ, tmG;
@@ -415,7 +421,7 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
   Decomp d{};
   d.tiles_n = tiles_n;
   d.nchunks = nchunks;
-  int split = kSMs / tiles;
+  int split = kSMs * MINB / tiles;
   if (split > a.max_split) split = a.max_split;
   if (split > nchunks) split = nchunks;
   if (split < 1) split = 1;
@@ -437,7 +443,7 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
   }
   const int64_t part_stride = (int64_t)a.M * a.ldc;
   const size_t smem = STAGES * (BM + BN) * 128 + 2 * STAGES * 8 + 1024;
-  auto kern = k_gtq<MT, NT, WM, WN, STAGES>;
+  auto kern = k_gtq<MT, NT, WM, WN, STAGES, MINB>;
   if (int e = set_smem(kern, smem)) return e;
   kern<<<units, (WM * WN + 1) * 32, smem, st>>>(tmQ, tmG, a.C, a.ldc, a.scratch, part_stride,
                                                  (int)a.M, (int)a.N, d);
