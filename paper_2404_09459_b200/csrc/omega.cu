@@ -10,10 +10,12 @@
 //  k_zig_attempt : every raw position p (128-bit LCG jump-ahead per thread)
 //                  evaluates the attempt that would START at p: accepted?,
 //                  value, raw draws consumed. Fast attempts (~99%) consume 1.
-//  k_zig_walk    : one thread per stream walks the attempt chain, visiting
-//                  only the rare "special" positions (tile-compacted lists),
-//                  marks positions swallowed by multi-draw attempts and
-//                  counts emitted normals per tile.
+//  k_zig_walk_*  : the attempt chain, visiting only the rare "special"
+//                  positions (tile-compacted lists): every tile walked in
+//                  parallel from carry-in 0, then a per-stream carry pass
+//                  re-walks the rare tiles entered mid-attempt; marks
+//                  positions swallowed by multi-draw attempts and counts
+//                  emitted normals per tile.
 //  k_zig_scatter : per tile, emitted flags -> prefix -> output index; writes
 //                  Omega^T (kp x ld) directly in the layout the sketch GEMM
 //                  consumes (value #e of the stream is Omega[e / k][e % k]).
@@ -270,68 +272,116 @@ __global__ void __launch_bounds__(kZigThreads) k_zig_attempt(
   }
 }
 
-// One warp per stream follows the attempt chain through the specials. The
-// tile's compact special records (offset | consumed << 10 | accepted << 31)
-// are staged in shared memory by the warp; lane 0 walks them. Positions that
-// emit nothing -- rejected starts and draws swallowed by multi-draw attempts
-// -- are recorded per tile as half-open intervals [a, b) of tile offsets;
-// the per-tile emit count is the tile length minus their total length.
+// The attempt chain through the specials is sequential only through its
+// carry: how far the last attempt of tile t reaches into tile t+1 (almost
+// always 0 -- a multi-draw attempt must start in the last few positions).
+// So every tile is walked in parallel assuming carry-in 0 (k_zig_walk_tiles,
+// one warp per (tile, stream)), and one warp per stream then runs the carry
+// chain over the per-tile carry-outs, re-walking only the rare tiles whose
+// actual carry-in is not 0 (k_zig_walk_fix). The result is identical to one
+// sequential walk. Positions that emit nothing -- rejected starts and draws
+// swallowed by multi-draw attempts -- are recorded per tile as half-open
+// intervals [a, b) of tile offsets; the per-tile emit count is the tile
+// length minus their total length.
 constexpr int kZigMaxIv = 64;  // intervals per tile (overflow -> status bit)
 
-__global__ void __launch_bounds__(32) k_zig_walk(int nstreams, int ntiles, int64_t P,
-                                                 int64_t nvals, const int* __restrict__ tile_nspec,
-                                                 const uint32_t* __restrict__ tile_spec,
-                                                 int* __restrict__ tile_emit,
-                                                 int* __restrict__ tile_niv,
-                                                 uint32_t* __restrict__ tile_iv,
-                                                 int* __restrict__ status) {
-  const int s = blockIdx.x;
-  const int lane = threadIdx.x;
+// Walk tile t of stream s from carry-in `cin` (positions t0 .. t0+cin-1 are
+// swallowed by the previous tile's attempt). Single thread; records in rec.
+// Writes the tile's interval list / emit count; returns the carry-out.
+RGSV_DI int64_t zig_walk_tile(const uint32_t* rec, int nsp, int64_t t0, int64_t t1, int64_t cin,
+                              uint32_t* iv_out, int* niv_out, int* emit_out, bool* overflow) {
+  int niv = 0, removed = 0;
+  int64_t covered = t0 + cin;
+  auto add = [&](int64_t a, int64_t b) {  // clip to this tile
+    if (a < t0) a = t0;
+    if (b > t1) b = t1;
+    if (b <= a) return;
+    const uint32_t ia = (uint32_t)(a - t0), ib = (uint32_t)(b - t0);
+    if (niv < kZigMaxIv) {
+      iv_out[niv++] = (ia << 16) | ib;
+    } else {
+      *overflow = true;
+    }
+    removed += (int)(ib - ia);
+  };
+  if (cin > 0) add(t0, covered);
+  for (int i = 0; i < nsp; ++i) {
+    const uint32_t r = rec[i];
+    const int64_t p = t0 + (r & 1023u);
+    if (p < covered) continue;  // swallowed: not an attempt start
+    const int consumed = (int)((r >> 10) & 0x3fffu);
+    const bool acc = (r >> 31) & 1u;
+    add(acc ? p + 1 : p, p + consumed);
+    covered = p + consumed;
+  }
+  *niv_out = niv;
+  *emit_out = (int)(t1 - t0) - removed;
+  return covered > t1 ? covered - t1 : 0;
+}
+
+__global__ void __launch_bounds__(32) k_zig_walk_tiles(int ntiles, int64_t P,
+                                                       const int* __restrict__ tile_nspec,
+                                                       const uint32_t* __restrict__ tile_spec,
+                                                       int* __restrict__ tile_emit,
+                                                       int* __restrict__ tile_niv,
+                                                       uint32_t* __restrict__ tile_iv,
+                                                       int* __restrict__ tile_cout) {
+  const int t = blockIdx.x, s = blockIdx.y, lane = threadIdx.x;
   __shared__ uint32_t rec[kZigTile];
-  __shared__ uint32_t iv[kZigMaxIv];
-  int64_t covered = 0;  // positions [0, covered) decided by the chain so far
-  int64_t total = 0;
-  bool overflow = false;
-  for (int t = 0; t < ntiles; ++t) {
+  const int64_t id = (int64_t)s * ntiles + t;
+  const int nsp = tile_nspec[id];
+  const uint32_t* ts = tile_spec + id * kZigTile;
+  for (int i = lane; i < nsp; i += 32) rec[i] = ts[i];
+  __syncwarp();
+  if (lane == 0) {
     const int64_t t0 = (int64_t)t * kZigTile;
     const int64_t t1 = t0 + kZigTile < P ? t0 + kZigTile : P;
-    const int nsp = tile_nspec[(int64_t)s * ntiles + t];
-    const uint32_t* ts = tile_spec + ((int64_t)s * ntiles + t) * kZigTile;
-    for (int i = lane; i < nsp; i += 32) rec[i] = ts[i];
-    __syncwarp();
-    if (lane == 0) {
-      int niv = 0, removed = 0;
-      auto add = [&](int64_t a, int64_t b) {  // clip to this tile
-        if (a < t0) a = t0;
-        if (b > t1) b = t1;
-        if (b <= a) return;
-        const uint32_t ia = (uint32_t)(a - t0), ib = (uint32_t)(b - t0);
-        if (niv < kZigMaxIv) {
-          iv[niv++] = (ia << 16) | ib;
-        } else {
-          overflow = true;
-        }
-        removed += (int)(ib - ia);
-      };
-      if (covered > t0) add(t0, covered);  // swallowed by the previous tile's attempt
-      for (int i = 0; i < nsp; ++i) {
-        const uint32_t r = rec[i];
-        const int64_t p = t0 + (r & 1023u);
-        if (p < covered) continue;  // swallowed: not an attempt start
-        const int consumed = (int)((r >> 10) & 0x3fffu);
-        const bool acc = (r >> 31) & 1u;
-        add(acc ? p + 1 : p, p + consumed);
-        covered = p + consumed;
+    int niv, emit;
+    bool overflow = false;
+    const int64_t cout = zig_walk_tile(rec, nsp, t0, t1, 0, tile_iv + id * kZigMaxIv, &niv, &emit,
+                                       &overflow);
+    tile_niv[id] = overflow ? -1 : niv;
+    tile_emit[id] = emit;
+    tile_cout[id] = (int)cout;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_zig_walk_fix(int ntiles, int64_t P, int64_t nvals,
+                                                     const int* __restrict__ tile_nspec,
+                                                     const uint32_t* __restrict__ tile_spec,
+                                                     int* __restrict__ tile_emit,
+                                                     int* __restrict__ tile_niv,
+                                                     uint32_t* __restrict__ tile_iv,
+                                                     const int* __restrict__ tile_cout,
+                                                     int* __restrict__ status) {
+  const int s = blockIdx.x, lane = threadIdx.x;
+  __shared__ uint32_t rec[kZigTile];
+  __shared__ int sh_cin;
+  int64_t cin = 0, total = 0;
+  bool overflow = false;
+  for (int t = 0; t < ntiles; ++t) {
+    const int64_t id = (int64_t)s * ntiles + t;
+    if (cin > 0) {  // rare: re-walk this tile from its true carry-in
+      const int nsp = tile_nspec[id];
+      const uint32_t* ts = tile_spec + id * kZigTile;
+      for (int i = lane; i < nsp; i += 32) rec[i] = ts[i];
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t t0 = (int64_t)t * kZigTile;
+        const int64_t t1 = t0 + kZigTile < P ? t0 + kZigTile : P;
+        int niv, emit;
+        sh_cin = (int)zig_walk_tile(rec, nsp, t0, t1, cin, tile_iv + id * kZigMaxIv, &niv, &emit,
+                                    &overflow);
+        tile_niv[id] = niv;
+        tile_emit[id] = emit;
       }
-      if (covered < t1) covered = t1;
-      tile_niv[(int64_t)s * ntiles + t] = niv;
-      uint32_t* out = tile_iv + ((int64_t)s * ntiles + t) * kZigMaxIv;
-      for (int i = 0; i < niv; ++i) out[i] = iv[i];
-      const int emit = (int)(t1 - t0) - removed;
-      tile_emit[(int64_t)s * ntiles + t] = emit;
-      total += emit;
+      __syncwarp();
+      cin = sh_cin;
+    } else {
+      cin = tile_cout[id];
+      if (tile_niv[id] < 0) overflow = true;
     }
-    __syncwarp();
+    total += tile_emit[id];
   }
   if (lane == 0 && (total < nvals || overflow)) atomicOr(status, RGSV_ST_OMEGA_SHORT);
 }
@@ -403,7 +453,7 @@ size_t omega_workspace_bytes(int nstreams, int64_t nvals) {
   b += (size_t)nstreams * sizeof(ZigStream) + 256;
   b += (size_t)nstreams * P * sizeof(double) + 256;
   b += (size_t)nstreams * P * sizeof(uint16_t) + 256;
-  b += (size_t)nstreams * ntiles * sizeof(int) * 3 + 768;
+  b += (size_t)nstreams * ntiles * sizeof(int) * 4 + 1024;
   b += (size_t)nstreams * ntiles * kZigTile * sizeof(uint32_t) + 256;
   b += (size_t)nstreams * ntiles * kZigMaxIv * sizeof(uint32_t) + 256;
   return b;
@@ -431,6 +481,7 @@ int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double
   int* tnspec = reinterpret_cast<int*>(take((size_t)nstreams * ntiles * sizeof(int)));
   int* temit = reinterpret_cast<int*>(take((size_t)nstreams * ntiles * sizeof(int)));
   int* tniv = reinterpret_cast<int*>(take((size_t)nstreams * ntiles * sizeof(int)));
+  int* tcout = reinterpret_cast<int*>(take((size_t)nstreams * ntiles * sizeof(int)));
   uint32_t* tspec =
       reinterpret_cast<uint32_t*>(take((size_t)nstreams * ntiles * kZigTile * sizeof(uint32_t)));
   uint32_t* tiv =
@@ -440,8 +491,10 @@ int omega_generate(const uint64_t* seeds, int nstreams, int64_t n, int k, double
   dim3 grid(ntiles, nstreams);
   k_zig_attempt<<<grid, kZigThreads, 0, st>>>(streams, P, val, code, tnspec, tspec);
   note_launch();
-  k_zig_walk<<<nstreams, 32, 0, st>>>(nstreams, ntiles, P, nall, tnspec, tspec, temit, tniv,
-                                      tiv, status);
+  k_zig_walk_tiles<<<grid, 32, 0, st>>>(ntiles, P, tnspec, tspec, temit, tniv, tiv, tcout);
+  note_launch();
+  k_zig_walk_fix<<<nstreams, 32, 0, st>>>(ntiles, P, nall, tnspec, tspec, temit, tniv, tiv, tcout,
+                                          status);
   note_launch();
   k_zig_scatter<<<grid, kZigThreads, 0, st>>>(P, val, temit, tniv, tiv, nvals, k, out, ldo,
                                               out_stride, offset);
