@@ -539,9 +539,229 @@ int chol_profile(const double* gram, int k, int kp, double* linv, long long* pro
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
+// ------------------------------------------- 16-wide blocked, kp <= 64
+// Diagonal 16x16 blocks are factored by ONE warp, register resident
+// (lane i holds row i; symmetric Gauss-Jordan on [A_JJ | I] yields L_JJ^T in
+// the A half and L_JJ^-1 in the X half, critical path one shuffle + rsqrt +
+// FMA per column). Panel L_IJ = A_IJ L_JJ^-T and trailing A_IK -= L_IJ L_KJ^T
+// are DMMA tiles spread over 8 warps; L^-1 is then assembled block row by
+// block row, W_IK = -W_II sum_{M=K}^{I-1} L_IM W_MK. Shared memory: A and W,
+// kp x (kp + 4) each (pitch 68 keeps both DMMA fragment patterns at two
+// wavefronts).
+constexpr int kCB = 16;
+
+__device__ void gj_block16(double* A, int lda, double* W, int ldw, int r0, double* rdiag,
+                           double* rdiag_acc, int k, int* fail) {
+  const int lane = threadIdx.x & 31;
+  double z[kCB], x[kCB];
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) {
+    z[c] = (lane < kCB) ? A[(r0 + lane) * lda + r0 + c] : (lane == c ? 1.0 : 0.0);
+    x[c] = (lane == c) ? 1.0 : 0.0;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < kCB; ++j) {
+    const double d = __shfl_sync(0xffffffffu, z[j], j);
+    double pa[kCB], px[kCB];
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) {
+      if (c > j) pa[c] = __shfl_sync(0xffffffffu, z[c], j);
+      if (c <= j) px[c] = __shfl_sync(0xffffffffu, x[c], j);
+    }
+    bad |= !(d > 0.0) || !isfinite(d);
+    const double r = rsqrt(d);
+    const double ff = (lane > j) ? z[j] * (r * r) : 0.0;
+    const double mul = (lane == j) ? r : 1.0;
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) {
+      if (c > j) z[c] = fma(-ff, pa[c], z[c]) * mul;
+      if (c <= j) x[c] = fma(-ff, px[c], x[c]) * mul;
+    }
+    z[j] = (lane > j) ? 0.0 : (lane == j ? d * r : z[j]);
+  }
+  if (lane < kCB) {
+    // lane j: z[c] (c >= j) = L[c][j]; x[c] (c <= j) = Linv[j][c]
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) {
+      A[(r0 + c) * lda + r0 + lane] = (c >= lane) ? z[c] : 0.0;  // L_JJ column `lane`
+      W[(r0 + lane) * ldw + r0 + c] = (c <= lane) ? x[c] : 0.0;  // Linv_JJ row `lane`
+    }
+    const int i = r0 + lane;
+    double dj = 0.0;
+#pragma unroll
+    for (int c = 0; c < kCB; ++c)
+      if (c == lane) dj = z[c];
+    if (i < k) {
+      if (rdiag) rdiag[i] = dj;
+      if (rdiag_acc) rdiag_acc[i] *= dj;
+    }
+  }
+  if (bad && lane == 0) *fail = 1;
+}
+
+__global__ void __launch_bounds__(256) k_chol_b16(const double* __restrict__ gram, int k, int kp,
+                                                  int64_t shift_rows, double* __restrict__ linv,
+                                                  double* __restrict__ rinv,
+                                                  double* __restrict__ r_upper,
+                                                  double* __restrict__ rdiag,
+                                                  double* __restrict__ rdiag_acc,
+                                                  int* __restrict__ status) {
+  extern __shared__ double smc[];
+  const int ld = kp + 4;
+  double* A = smc;           // kp x ld : A -> L (lower, diag blocks full)
+  double* W = A + kp * ld;   // kp x ld : L^-1
+  __shared__ int fail;
+  __shared__ double shift;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = kp / kCB;
+  for (int e = tid; e < kp * kp; e += blockDim.x) {
+    const int i = e / kp, c = e % kp;
+    A[i * ld + c] = (i < k && c < k) ? gram[(int64_t)i * kp + c] : (i == c ? 1.0 : 0.0);
+    W[i * ld + c] = 0.0;
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  if (shift_rows > 0) {
+    if (warp == 0) {  // trace from shared memory, fixed-order warp reduction
+      double tr = 0.0;
+      for (int i = lane; i < k; i += 32) tr += A[i * ld + i];
+      tr = warp_sum(tr);
+      if (lane == 0) shift = 11.0 * ((double)shift_rows * k + (double)k * (k + 1)) * 0x1p-53 * tr;
+    }
+    __syncthreads();
+    for (int i = tid; i < k; i += blockDim.x) A[i * ld + i] += shift;
+    __syncthreads();
+  }
+  const int g = lane >> 2, t = lane & 3;
+  for (int J = 0; J < nb; ++J) {
+    const int r0 = J * kCB;
+    if (warp == 0) gj_block16(A, ld, W, ld, r0, rdiag, rdiag_acc, k, &fail);
+    __syncthreads();
+    // panel: L_IJ = A_IJ W_JJ^T for I > J (8x8 output tiles)
+    const int prow = kp - r0 - kCB;  // rows below the diagonal block
+    const int ntile = (prow / 8) * 2;  // <= 12 for kp <= 64: two slots per warp
+    double pv[2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int u = warp + 8 * q;
+      if (u < ntile) {
+        const int rr = r0 + kCB + (u >> 1) * 8, cc = (u & 1) * 8;
+        double c2[2] = {0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < kCB / 4; ++ks)
+          dmma(c2, A[(rr + g) * ld + r0 + ks * 4 + t], W[(r0 + cc + g) * ld + r0 + ks * 4 + t]);
+        pv[q][0] = c2[0];
+        pv[q][1] = c2[1];
+      }
+    }
+    __syncthreads();  // every read of A_IJ done before the in-place write
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int u = warp + 8 * q;
+      if (u < ntile) {
+        const int rr = r0 + kCB + (u >> 1) * 8, cc = (u & 1) * 8;
+        A[(rr + g) * ld + r0 + cc + 2 * t] = pv[q][0];
+        A[(rr + g) * ld + r0 + cc + 2 * t + 1] = pv[q][1];
+      }
+    }
+    __syncthreads();
+    // trailing: A_IK -= L_IJ L_KJ^T, 8x8 tiles (row tile >= col tile block-wise)
+    const int tb = (kp - r0 - kCB) / 8;  // 8-tiles in the trailing dimension
+    for (int u = warp; u < tb * tb; u += 8) {
+      const int ti = u / tb, tk = u % tb;
+      if ((ti >> 1) < (tk >> 1)) continue;  // strictly upper 16-blocks not needed
+      const int rr = r0 + kCB + ti * 8, cc = r0 + kCB + tk * 8;
+      double c2[2] = {A[(rr + g) * ld + cc + 2 * t], A[(rr + g) * ld + cc + 2 * t + 1]};
+      double m2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < kCB / 4; ++ks)
+        dmma(m2, A[(rr + g) * ld + r0 + ks * 4 + t], A[(cc + g) * ld + r0 + ks * 4 + t]);
+      A[(rr + g) * ld + cc + 2 * t] = c2[0] - m2[0];
+      A[(rr + g) * ld + cc + 2 * t + 1] = c2[1] - m2[1];
+    }
+    __syncthreads();
+  }
+  // L^-1 off-diagonal blocks, block row by block row
+  for (int I = 1; I < nb; ++I) {
+    // T_K = sum_{M=K}^{I-1} L_IM W_MK for K < I, staged in W_IK
+    for (int u = warp; u < I * 4; u += 8) {
+      const int K = u >> 2, q = u & 3;
+      const int rr = I * kCB + (q >> 1) * 8, cc = K * kCB + (q & 1) * 8;
+      double c2[2] = {0.0, 0.0};
+      for (int M = K; M < I; ++M)
+#pragma unroll
+        for (int ks = 0; ks < kCB / 4; ++ks)
+          dmma(c2, A[(rr + g) * ld + M * kCB + ks * 4 + t],
+               W[(M * kCB + ks * 4 + t) * ld + cc + g]);
+      W[(rr + g) * ld + cc + 2 * t] = c2[0];
+      W[(rr + g) * ld + cc + 2 * t + 1] = c2[1];
+    }
+    __syncthreads();
+    // W_IK = -W_II T_K  (I * 4 <= 12 tiles: two slots per warp)
+    double ov[2][2];
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int u = warp + 8 * s2;
+      if (u < I * 4) {
+        const int K = u >> 2, q = u & 3;
+        const int rr = I * kCB + (q >> 1) * 8, cc = K * kCB + (q & 1) * 8;
+        double c2[2] = {0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < kCB / 4; ++ks)
+          dmma(c2, W[(rr + g) * ld + I * kCB + ks * 4 + t],
+               W[(I * kCB + ks * 4 + t) * ld + cc + g]);
+        ov[s2][0] = -c2[0];
+        ov[s2][1] = -c2[1];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int u = warp + 8 * s2;
+      if (u < I * 4) {
+        const int K = u >> 2, q = u & 3;
+        const int rr = I * kCB + (q >> 1) * 8, cc = K * kCB + (q & 1) * 8;
+        W[(rr + g) * ld + cc + 2 * t] = ov[s2][0];
+        W[(rr + g) * ld + cc + 2 * t + 1] = ov[s2][1];
+      }
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) atomicOr(status, RGSV_ST_CHOL_BREAKDOWN);
+    for (int e = tid; e < kp * kp; e += blockDim.x) {
+      linv[e] = __longlong_as_double(0x7ff8000000000000LL);
+      if (rinv) rinv[e] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+    return;
+  }
+  for (int e = tid; e < kp * kp; e += blockDim.x) {
+    const int i = e / kp, c = e % kp;
+    const double v = (c <= i) ? W[i * ld + c] : 0.0;
+    linv[e] = v;
+    if (rinv) rinv[(int64_t)c * kp + i] = v;
+    if (r_upper) r_upper[(int64_t)c * kp + i] = (c <= i) ? A[i * ld + c] : 0.0;  // R = L^T
+  }
+}
+
 int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
              double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st) {
   if (k <= 0 || kp < k || kp % 16 != 0 || kp > 1024) return RGSV_ERR_DIMENSION;
+  if (kp <= 64 && !getenv("RGSV_CHOL_BLK")) {
+    const size_t bytes = (size_t)2 * kp * (kp + 4) * sizeof(double);
+    static bool attr_b16 = false;
+    if (!attr_b16) {
+      if (cudaFuncSetAttribute(k_chol_b16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)((size_t)2 * 64 * 68 * sizeof(double))) != cudaSuccess)
+        return RGSV_ERR_CUDA;
+      attr_b16 = true;
+    }
+    k_chol_b16<<<1, 256, bytes, st>>>(gram, k, kp, shift_rows, linv, rinv, r_upper, rdiag,
+                                      rdiag_acc, status);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+  }
   if (kp <= 128) {
     const size_t bytes = ((size_t)kp * (kp + 4) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
     static bool attr_blk = false;
