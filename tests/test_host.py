@@ -88,3 +88,116 @@ def test_workload_generator():
     assert s[19] > 1e3 * s[20]  # rank-20 signal over 1e-8 noise
     assert CONFIGS["cfg1"].flops == 2.0 * 36000 * 1000 * 60 * 6
     assert CONFIGS["cfg3"].batch == 4096
+
+
+# ------------------------------------------------ routing and batch results
+def test_mode_routing():
+    """fixed-width -> fused pair pipeline; direct / adaptive -> general loop."""
+    from paper_2404_09459_b200.engine import _fixed_width
+
+    fixed = GsvOptions(extraction=ExtractionConfig.fixed_rank(30, 0, 1))
+    assert _fixed_width(fixed, 2000, 1500, 200) == (30, 30)
+    assert _fixed_width(GsvOptions(), 2000, 1500, 200) is None          # adaptive default
+    assert _fixed_width(GsvOptions(method="direct"), 20, 15, 30) is None  # no extraction
+    # direct ignores max_cols like the reference (engine.py:246-249)
+    big = GsvOptions(method="direct", extraction=ExtractionConfig(max_cols=500))
+    assert _fixed_width(big, 20, 15, 30) is None
+    with pytest.raises(ValidationError):
+        _fixed_width(GsvOptions(extraction=ExtractionConfig(max_cols=500)), 20, 15, 30)
+
+
+class _FakePlan:
+    def __init__(self, B, n, k):
+        self.B, self.n, self.k = B, n, k
+        self.res_stride = 6 * n + 4 + 2 * k
+
+
+def _fake_batch(B=3, n=8, k=2):
+    """Host buffers laid out like rgsv_batch_gsvd's outputs (F2 spectra)."""
+    plan = _FakePlan(B, n, k)
+    rs = plan.res_stride
+    fh = np.zeros(B * rs + 4 * B)
+    ih = np.zeros(5 * B, dtype=np.int32)
+    for j in range(B):
+        o = fh[j * rs:(j + 1) * rs]
+        o[:k] = 1.0                      # alphas
+        o[n + k:2 * n] = 1.0             # betas
+        o[2 * n:2 * n + k] = np.inf      # rho
+        o[4 * n:4 * n + k] = 1.0 / k     # p1
+        o[5 * n + k:6 * n] = 1.0 / (n - k)
+        o[6 * n:6 * n + 4] = [math.log(k) / math.log(n), math.log(n - k) / math.log(n), 1, 1]
+        o[6 * n + 4:6 * n + 4 + 2 * k] = 1.0
+        ih[4 * j:4 * j + 4] = [k, k, k, 0]
+        fh[B * rs + 4 * j:B * rs + 4 * j + 4] = [10.0 + j, 4.0, 9.0, 2.0]
+    return fh, ih, plan
+
+
+def test_small_batch_runs_vectorized_validation():
+    from paper_2404_09459_b200.engine import SmallBatchRuns
+
+    fh, ih, plan = _fake_batch()
+    runs = SmallBatchRuns(fh, ih, plan, GsvOptions(extraction=ExtractionConfig.fixed_rank(2)))
+    assert len(runs) == 3
+    r1 = runs[1]
+    assert (r1.r, r1.s) == (2, 0) and np.array_equal(r1.alphas, [1, 1, 0, 0, 0, 0, 0, 0])
+    assert r1.basis1.residual_history == [math.sqrt(11.0), math.sqrt(7.0)]
+    assert r1.d1 == pytest.approx(math.log(2) / math.log(8))
+    assert [r.r for r in runs[0:3]] == [2, 2, 2] and runs[-1].r == 2
+    with pytest.raises(IndexError):
+        runs[3]
+
+
+@pytest.mark.parametrize("corrupt,exc", [
+    ("pythagoras", ValidationError),
+    ("order", ValidationError),
+    ("unsnapped", ValidationError),
+    ("chol", "RankDeficiencyError"),
+    ("jacobi", "ConvergenceError"),
+    ("nonfinite", ValidationError),
+])
+def test_small_batch_runs_reject(corrupt, exc):
+    import paper_2404_09459_b200 as rg
+    from paper_2404_09459_b200.engine import SmallBatchRuns
+
+    fh, ih, plan = _fake_batch()
+    n, rs = plan.n, plan.res_stride
+    o = fh[rs:2 * rs]
+    if corrupt == "pythagoras":
+        o[n + 3] = 0.5
+    elif corrupt == "order":
+        o[1], o[2] = 0.5, 0.9
+        o[n + 1], o[n + 2] = math.sqrt(0.75), math.sqrt(1 - 0.81)
+    elif corrupt == "unsnapped":
+        o[n + 0] = 1e-300  # classified-zero beta that is not exactly 0
+        o[0] = math.sqrt(1 - 1e-600)
+    elif corrupt == "chol":
+        ih[4 * 3 + 1] = 0x1
+    elif corrupt == "jacobi":
+        ih[4 * 3 + 2] = 0x4
+    elif corrupt == "nonfinite":
+        fh[3 * rs + 4] = np.nan
+    exc = getattr(rg, exc) if isinstance(exc, str) else exc
+    with pytest.raises(exc):
+        SmallBatchRuns(fh, ih, plan, GsvOptions(extraction=ExtractionConfig.fixed_rank(2)))
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference prints one JSON line with the contract keys
+    (the oracle port timed on the host cores)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--config", "cfg0", "--steps", "2", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "cpu_baseline", "e2e", "impl"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
