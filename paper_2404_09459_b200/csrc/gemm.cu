@@ -334,9 +334,9 @@ int set_smem(K kernel, size_t bytes) {
   return 0;
 }
 
-// (2 CTAs/SM with a 4-stage ring was measured slower on the cfg1 shapes:
-// gtq 109 vs 99 us, gx 149 vs 90 us -- tools/gemm_ab.py; MINB stays a
-// template knob.)
+// Tile-shape experiments on the cfg1 shapes (tools/gemm_ab.py), both slower
+// than the configurations below: 2 CTAs/SM with a 4-stage ring (gtq 109 vs
+// 99 us, gx 149 vs 90 us) and 12 DMMA warps per CTA (gtq 105, gx 111 us).
 // Plan the unit list for `tiles` output tiles over `nchunks` K chunks.
 Decomp plan_units(int tiles_m, int tiles_n, int nchunks, int max_split, int* units, int* S,
                   int per_sm = 1) {
