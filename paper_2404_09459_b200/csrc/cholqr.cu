@@ -550,6 +550,12 @@ int chol_profile(const double* gram, int k, int kp, double* linv, long long* pro
 // wavefronts).
 constexpr int kCB = 16;
 
+RGSV_DI double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __device__ void gj_block16(double* A, int lda, double* W, int ldw, int r0, double* rdiag,
                            double* rdiag_acc, int k, int* fail) {
   const int lane = threadIdx.x & 31;
@@ -621,7 +627,87 @@ __global__ void __launch_bounds__(256) k_chol_b16(const double* __restrict__ gra
     W[i * ld + c] = 0.0;
   }
   if (tid == 0) fail = 0;
+  __shared__ int near_id;
+  if (tid == 0) near_id = 0;
   __syncthreads();
+  if (shift_rows == 0) {
+    // Near-identity Gram (the third CholeskyQR pass: G = I + E, |E| ~ u
+    // cond(Q1)^2): L = I + X with X = Phi(E - X1 X1^T), X1 = Phi(E) (Phi:
+    // strict lower + half diagonal) and L^-1 = I - X + X^2, exact in fp64
+    // for max|E| <= 1e-6 (neglected terms O(|E|^3) <= 1e-18); no pivot chain.
+    double mx = 0.0;
+    for (int e = tid; e < k * k; e += blockDim.x) {
+      const int i = e / k, c = e % k;
+      mx = fmax(mx, fabs(A[i * ld + c] - (i == c ? 1.0 : 0.0)));
+    }
+    mx = warp_max(mx);
+    __shared__ double wm[8];
+    if (lane == 0) wm[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+      near_id = (m <= 1e-6) ? 1 : 0;
+    }
+    __syncthreads();
+  }
+  if (near_id) {
+    const int g = lane >> 2, t = lane & 3;
+    const int nt8 = kp / 8;
+    // A := E (padding 0); W := X1 = Phi(E)
+    for (int e = tid; e < kp * kp; e += blockDim.x) {
+      const int i = e / kp, c = e % kp;
+      const double ev = A[i * ld + c] - (i == c ? 1.0 : 0.0);
+      A[i * ld + c] = ev;
+      W[i * ld + c] = (c < i) ? ev : (c == i ? 0.5 * ev : 0.0);
+    }
+    __syncthreads();
+    // A := E - X1 X1^T (lower 8x8 tiles)
+    for (int u = warp; u < nt8 * nt8; u += 8) {
+      const int ti = u / nt8, tc = u % nt8;
+      if (tc > ti) continue;
+      double m2[2] = {0.0, 0.0};
+      for (int ks = 0; ks < kp / 4; ++ks)
+        dmma(m2, W[(ti * 8 + g) * ld + ks * 4 + t], W[(tc * 8 + g) * ld + ks * 4 + t]);
+      A[(ti * 8 + g) * ld + tc * 8 + 2 * t] -= m2[0];
+      A[(ti * 8 + g) * ld + tc * 8 + 2 * t + 1] -= m2[1];
+    }
+    __syncthreads();
+    // W := X = Phi(A)
+    for (int e = tid; e < kp * kp; e += blockDim.x) {
+      const int i = e / kp, c = e % kp;
+      W[i * ld + c] = (c < i) ? A[i * ld + c] : (c == i ? 0.5 * A[i * ld + c] : 0.0);
+    }
+    __syncthreads();
+    // A := L^-1 = I - X + X^2 (lower tiles; X lower triangular)
+    for (int u = warp; u < nt8 * nt8; u += 8) {
+      const int ti = u / nt8, tc = u % nt8;
+      double m2[2] = {0.0, 0.0};
+      if (tc <= ti)
+        for (int ks = 0; ks < kp / 4; ++ks)
+          dmma(m2, W[(ti * 8 + g) * ld + ks * 4 + t], W[(ks * 4 + t) * ld + tc * 8 + g]);
+      const int i = ti * 8 + g, c0 = tc * 8 + 2 * t;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = c0 + h;
+        A[i * ld + c] = (c <= i) ? ((i == c ? 1.0 : 0.0) - W[i * ld + c] + m2[h]) : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < kp * kp; e += blockDim.x) {
+      const int i = e / kp, c = e % kp;
+      const double v = A[i * ld + c];
+      linv[e] = v;
+      if (rinv) rinv[(int64_t)c * kp + i] = v;
+      if (r_upper) r_upper[(int64_t)c * kp + i] = (i == c ? 1.0 : 0.0) + W[i * ld + c];
+    }
+    for (int i = tid; i < k; i += blockDim.x) {
+      const double di = 1.0 + W[i * ld + i];
+      if (rdiag) rdiag[i] = di;
+      if (rdiag_acc) rdiag_acc[i] *= di;
+    }
+    return;
+  }
   if (shift_rows > 0) {
     if (warp == 0) {  // trace from shared memory, fixed-order warp reduction
       double tr = 0.0;

@@ -172,3 +172,28 @@ def test_comparative_kernel_vs_oracle():
     assert np.max(np.abs(h[3 * n:4 * n] - theta)) <= 1e-15
     assert np.max(np.abs(h[4 * n:5 * n] - p1)) <= 1e-15
     assert abs(h[6 * n] - d1) <= 1e-14 and abs(h[6 * n + 1] - d2) <= 1e-14
+
+
+@pytest.mark.parametrize("k,scale", [(60, 1e-8), (30, 3e-7), (64, 1e-10), (16, 0.0)])
+def test_chol_inv_near_identity_path(k, scale):
+    """Third CholeskyQR pass: Gram = I + E, |E| small -> expansion path; must
+    equal the Cholesky inverse to fp64 roundoff."""
+    kp = (k + 15) // 16 * 16
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((k, k))
+    e = scale * (x + x.T)
+    a = np.eye(k) + e
+    G = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")
+    G[:k, :k] = torch.from_numpy(a)
+    linv = torch.zeros(kp * kp + kp * (kp + 1), dtype=torch.float64, device="cuda")
+    rinv = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")
+    rd = torch.zeros(kp, dtype=torch.float64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _native.check(_native.lib().rgsv_chol_inv(dev.vp(G), k, kp, 0, dev.vp(linv), dev.vp(rinv),
+                                              dev.vp(rd), dev.vp(status), _st()), "chol")
+    li = linv[: kp * kp].view(kp, kp).cpu().numpy()
+    ref = np.linalg.inv(np.linalg.cholesky(a))
+    assert np.max(np.abs(li[:k, :k] - ref)) <= 1e-15
+    assert np.array_equal(li[k:, k:], np.eye(kp - k)) and not np.any(li[:k, k:])
+    assert np.max(np.abs(rd.cpu().numpy()[:k] - np.diag(np.linalg.cholesky(a)))) <= 1e-15
+    assert np.array_equal(rinv.cpu().numpy(), li.T)
