@@ -367,6 +367,7 @@ struct Chain {
   RGSV_DI void chol(int k, int64_t shift_rows) {
     constexpr int LD = KP + 1;
     static_assert(KP <= 32, "one lane per row");
+    if (shift_rows == 0 && near_identity_inverse(k)) return;
     if (warp == 0) {
       const bool row_ok = lane < k;
       double a[KP], x[KP];
@@ -417,6 +418,66 @@ struct Chain {
       }
     }
     __syncthreads();
+  }
+
+  // ---- third CholeskyQR pass: gram = I + E with max|E| <= 1e-6 ->
+  //      L^-1 = I - X + X^2, X = Phi(E - X1 X1^T), X1 = Phi(E) (Phi: strict
+  //      lower + half diagonal); exact in fp64 (neglected terms O(|E|^3)).
+  //      Returns false (nothing written) when the Gram is not that close.
+  RGSV_DI bool near_identity_inverse(int k) {
+    constexpr int LD = KP + 1;
+    constexpr int NT8 = KP / 8;
+    double mx = 0.0;
+    for (int e = tid; e < KP * KP; e += kThreads) {
+      const int i = e / KP, c = e % KP;
+      if (i < k && c < k) mx = fmax(mx, fabs(gram[i * LD + c] - (i == c ? 1.0 : 0.0)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) wred[warp * 64 + 2] = mx;
+    __syncthreads();
+    double m = 0.0;
+    for (int w = 0; w < kWarps; ++w) m = fmax(m, wred[w * 64 + 2]);
+    if (!(m <= 1e-6)) return false;  // uniform across the CTA
+    const int g = lane >> 2, t = lane & 3;
+    // lmat := X1 = Phi(E), gram := E (padding 0)
+    for (int e = tid; e < KP * KP; e += kThreads) {
+      const int i = e / KP, c = e % KP;
+      const double ev = (i < k && c < k) ? gram[i * LD + c] - (i == c ? 1.0 : 0.0) : 0.0;
+      gram[i * LD + c] = ev;
+      lmat[i * LD + c] = (c < i) ? ev : (c == i ? 0.5 * ev : 0.0);
+    }
+    __syncthreads();
+    if (warp < NT8 * NT8) {  // gram := E - X1 X1^T
+      const int ti = warp / NT8, tc = warp % NT8;
+      double m2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < KP / 4; ++ks)
+        dmma(m2, lmat[(ti * 8 + g) * LD + ks * 4 + t], lmat[(tc * 8 + g) * LD + ks * 4 + t]);
+      gram[(ti * 8 + g) * LD + tc * 8 + 2 * t] -= m2[0];
+      gram[(ti * 8 + g) * LD + tc * 8 + 2 * t + 1] -= m2[1];
+    }
+    __syncthreads();
+    for (int e = tid; e < KP * KP; e += kThreads) {  // lmat := X = Phi(gram)
+      const int i = e / KP, c = e % KP;
+      lmat[i * LD + c] = (c < i) ? gram[i * LD + c] : (c == i ? 0.5 * gram[i * LD + c] : 0.0);
+    }
+    __syncthreads();
+    if (warp < NT8 * NT8) {  // linv := I - X + X^2
+      const int ti = warp / NT8, tc = warp % NT8;
+      double m2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < KP / 4; ++ks)
+        dmma(m2, lmat[(ti * 8 + g) * LD + ks * 4 + t], lmat[(ks * 4 + t) * LD + tc * 8 + g]);
+      const int i = ti * 8 + g;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tc * 8 + 2 * t + h;
+        linv[i * LD + c] = (c <= i) ? ((i == c ? 1.0 : 0.0) - lmat[i * LD + c] + m2[h]) : 0.0;
+      }
+    }
+    __syncthreads();
+    return true;
   }
 
   // ---- buf (rows x KP, swizzled) <- buf L^-T, in place, warp per 8 rows
