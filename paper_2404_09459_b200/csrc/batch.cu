@@ -112,16 +112,25 @@ struct ChainArgs {
   int yrows;            // shared-memory rows of the Y slice (multiple of 32)
 };
 
+// G tiles: kTR x NP, unpadded, 16-byte chunk q of row r stored at
+// q ^ ((r & 3) << 1) (stays inside its 128-byte segment): the A fragments of
+// Y = G X (8 rows x 4 cols) and of G^T Q (4 rows x 8 cols) both hit the
+// minimum two wavefronts.
+template <int NP>
+RGSV_DI int gx_idx(int r, int c) {
+  return r * NP + ((((c >> 1) ^ ((r & 3) << 1))) << 1) + (c & 1);
+}
+
 template <int NP, int KP>
 struct Layout {
-  static constexpr int GP = NP + 4;                 // G tile pitch (doubles)
-  static constexpr int kG = kStages * kTR * GP;     // G ring
+  static constexpr int GP = NP + 4;                 // X^T pitch (doubles)
+  static constexpr int kG = kStages * kTR * NP;     // G ring (also holds zb + wred between passes)
   static constexpr int kX = KP * GP;                // X^T (KP x NP)
   static constexpr int kPart = NP * KP;             // one reduction slot
   static constexpr int kSmall = KP * (KP + 1);      // Gram / L / L^-1
+  static_assert(NP * KP + kWarps * 64 <= kG, "zb + wred must fit the idle G ring");
   static size_t bytes(int yrows) {
-    return sizeof(double) *
-           ((size_t)yrows * KP + kG + kX + 2 * kPart + NP * KP + 3 * kSmall + kWarps * 64 + 64);
+    return sizeof(double) * ((size_t)yrows * KP + kG + kX + 2 * kPart + 3 * kSmall + 64);
   }
 };
 
@@ -133,11 +142,11 @@ struct Chain {
   double* gst;   // G tile ring
   double* xt;    // X^T: KP x GP
   double* part;  // 2 reduction slots of NP*KP
-  double* zb;    // reduced Z (NP x KP, swizzled like ys)
+  double* zb;    // reduced Z / B^T (NP x KP), in the idle G ring
   double* gram;  // KP x (KP+1)
   double* lmat;  // KP x (KP+1): Cholesky factor, in place
   double* linv;  // KP x (KP+1): L^-1 (row-major)
-  double* wred;  // per-warp partials (kWarps x 64)
+  double* wred;  // per-warp partials (kWarps x 64), in the idle G ring
   double* misc;  // scalars
   int slot;
   int fail;
@@ -149,12 +158,12 @@ struct Chain {
     gst = ys + (size_t)yrows * KP;
     xt = gst + Lo::kG;
     part = xt + Lo::kX;
-    zb = part + 2 * Lo::kPart;
-    gram = zb + NP * KP;
+    gram = part + 2 * Lo::kPart;
     lmat = gram + Lo::kSmall;
     linv = lmat + Lo::kSmall;
-    wred = linv + Lo::kSmall;
-    misc = wred + kWarps * 64;
+    misc = linv + Lo::kSmall;
+    zb = gst;                  // G ring is idle whenever zb / wred are live
+    wred = gst + NP * KP;
     slot = 0;
     tid = threadIdx.x;
     lane = tid & 31;
@@ -186,7 +195,7 @@ struct Chain {
 
   // ---- stream this CTA's G rows [r0, r1) through the ring, tile by tile
   RGSV_DI void issue_tile(const BatchMat& g, int r0, int r1, int t, int n) {
-    double* dst = gst + (t % kStages) * kTR * GP;
+    double* dst = gst + (t % kStages) * kTR * NP;
     constexpr int kChunks = kTR * (NP / 2);
     for (int e = tid; e < kChunks; e += kThreads) {
       const int rr = e / (NP / 2), cc = (e % (NP / 2)) * 2;
@@ -194,7 +203,7 @@ struct Chain {
       int bytes = 0;
       if (row < r1 && cc < n) bytes = (cc + 1 < n) ? 16 : 8;
       const double* src = bytes ? g.g + (int64_t)row * g.ld + cc : g.g;
-      cp_async16(dst + rr * GP + cc, src, bytes);
+      cp_async16(dst + gx_idx<NP>(rr, cc), src, bytes);
     }
   }
 
@@ -212,7 +221,7 @@ struct Chain {
       __syncthreads();
       if (t + kStages - 1 < T) issue_tile(g, r0, r1, t + kStages - 1, n);
       cp_commit();
-      body(t, gst + (t % kStages) * kTR * GP);
+      body(t, gst + (t % kStages) * kTR * NP);
     }
     cp_wait<0>();
     __syncthreads();
@@ -238,11 +247,12 @@ struct Chain {
         const int b = warp + i * kWarps;
         const int rb = b % kRB, cb = b / kRB;
         double cc[4][2] = {};
-        const double* arow = gt + (rb * 8 + (lane >> 2)) * GP + (lane & 3);
+        const int ar = rb * 8 + (lane >> 2);
 #pragma unroll
         for (int ks = 0; ks < NP / 4; ks += 4) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dmma(cc[u], arow[(ks + u) * 4], xf[i][ks + u]);
+          for (int u = 0; u < 4; ++u)
+            dmma(cc[u], gt[gx_idx<NP>(ar, (ks + u) * 4 + (lane & 3))], xf[i][ks + u]);
         }
         double c[2] = {(cc[0][0] + cc[1][0]) + (cc[2][0] + cc[3][0]),
                        (cc[0][1] + cc[1][1]) + (cc[2][1] + cc[3][1])};
@@ -254,7 +264,7 @@ struct Chain {
       if (ss) {
         double a = 0.0;
         for (int e = tid; e < kTR * NP; e += kThreads) {
-          const double v = gt[(e / NP) * GP + (e % NP)];
+          const double v = gt[gx_idx<NP>(e / NP, e % NP)];
           a = fma(v, v, a);
         }
         *ss += a;
@@ -276,7 +286,7 @@ struct Chain {
 #pragma unroll
         for (int ks = 0; ks < kTR / 4; ++ks) {
           const int rr = ks * 4 + (lane & 3);
-          const double a = gt[rr * GP + ib * 8 + (lane >> 2)];
+          const double a = gt[gx_idx<NP>(rr, ib * 8 + (lane >> 2))];
           const double bv = ys[yx<KP>(t * kTR + rr, jb * 8 + (lane >> 2))];
           dmma(acc[i][ks & 1], a, bv);
         }
@@ -367,7 +377,16 @@ struct Chain {
   RGSV_DI void chol(int k, int64_t shift_rows) {
     constexpr int LD = KP + 1;
     static_assert(KP <= 32, "one lane per row");
-    if (shift_rows == 0 && near_identity_inverse(k)) return;
+#ifdef RGSV_BATCH_PROFILE
+    if (tid == 0) atomicAdd(&g_batch_prof[15], 1ull);
+    const long long _c0 = clock64();
+#endif
+    if (shift_rows == 0 && near_identity_inverse(k)) {
+#ifdef RGSV_BATCH_PROFILE
+      if (tid == 0) atomicAdd(&g_batch_prof[13], (unsigned long long)(clock64() - _c0));
+#endif
+      return;
+    }
     if (warp == 0) {
       const bool row_ok = lane < k;
       double a[KP], x[KP];
@@ -439,6 +458,9 @@ struct Chain {
     double m = 0.0;
     for (int w = 0; w < kWarps; ++w) m = fmax(m, wred[w * 64 + 2]);
     if (!(m <= 1e-6)) return false;  // uniform across the CTA
+#ifdef RGSV_BATCH_PROFILE
+    if (tid == 0) atomicAdd(&g_batch_prof[14], 1ull);
+#endif
     const int g = lane >> 2, t = lane & 3;
     // lmat := X1 = Phi(E), gram := E (padding 0)
     for (int e = tid; e < KP * KP; e += kThreads) {
@@ -562,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
     const int rpc = (rows + CS - 1) / CS;
     const int r0 = min(rows, (int)C.crank * rpc), r1 = min(rows, r0 + rpc);
     const int rl = r1 - r0;
-    const int rl32 = (rl + kTR - 1) / kTR * kTR;
+    const int rlt = (rl + kTR - 1) / kTR * kTR;
     C.fail = 0;
     PROF_T0();
     // X^T = Omega^T block (KP x n), zero-padded
@@ -592,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       C.reduce(1, [&](int, double s) { C.misc[0] = s; });
     }
     PROF(8);
-    C.cholqr3(C.ys, rl32, k, rows, true);
+    C.cholqr3(C.ys, rlt, k, rows, true);
     PROF(9);
     for (int it = 0; it < A.q; ++it) {
       // (2) Z = G^T Q (n x k), cluster-reduced, then Qhat = cholqr3(Z)
@@ -611,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       C.pass_gx(g, r0, r1, n, nullptr);
       __syncthreads();
       PROF(1);
-      C.cholqr3(C.ys, rl32, k, rows, true);
+      C.cholqr3(C.ys, rlt, k, rows, true);
       PROF(9);
     }
     // (4) B^T = G^T Q (n x k), cluster-reduced; rank 0 writes B and ||B||^2

@@ -47,3 +47,6 @@ nm = 2 * B
 for i, nmv in names.items():
     print(f"{nmv:28s} {buf[i] / tot * 100:5.1f}%  {buf[i] / nm / 4 / 1.9e3:8.2f} us/matrix/CTA")
 print(f"total {tot / nm / 4 / 1.9e3:.1f} us per matrix-chain per CTA (clock ~1.9 GHz)")
+print(f"chol calls {buf[15]}, near-identity fast path {buf[14]} "
+      f"({buf[13] / max(buf[14], 1) / 1.9e3:.2f} us each incl. the check); "
+      f"all chol phases {buf[6] / max(buf[15], 1) / 1.9e3:.2f} us per call")
