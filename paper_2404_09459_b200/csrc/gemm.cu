@@ -425,6 +425,23 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
   if (split > a.max_split) split = a.max_split;
   if (split > nchunks) split = nchunks;
   if (split < 1) split = 1;
+  // Long reductions (cfg2: 12500 K-chunks over 63 tiles): choose the split
+  // that fills whole waves best (63 x 2 = 126 of 148 SMs -> 63 x 7 = 441 of
+  // 444 slots), keeping >= 256 chunks per unit so the pipeline fill stays
+  // negligible; fewer splits win ties.
+  if (nchunks / 256 > split) {
+    const int slots = kSMs * MINB;
+    double best = (double)(tiles * split) / (double)(((tiles * split + slots - 1) / slots) * slots);
+    const int smax = nchunks / 256 < a.max_split ? nchunks / 256 : a.max_split;
+    for (int sp = split + 1; sp <= smax; ++sp) {
+      const int u = tiles * sp;
+      const double eff = (double)u / (double)(((u + slots - 1) / slots) * slots);
+      if (eff > best + 0.02) {
+        best = eff;
+        split = sp;
+      }
+    }
+  }
   int units = tiles, S = 0;
   if (split == 1) {
     d.full = tiles;
