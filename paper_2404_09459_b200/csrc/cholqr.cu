@@ -662,15 +662,28 @@ __global__ void __launch_bounds__(256) k_chol_b16(const double* __restrict__ gra
       W[i * ld + c] = (c < i) ? ev : (c == i ? 0.5 * ev : 0.0);
     }
     __syncthreads();
-    // A := E - X1 X1^T (lower 8x8 tiles)
-    for (int u = warp; u < nt8 * nt8; u += 8) {
-      const int ti = u / nt8, tc = u % nt8;
-      if (tc > ti) continue;
-      double m2[2] = {0.0, 0.0};
-      for (int ks = 0; ks < kp / 4; ++ks)
+    // lower 8x8 tiles (ti >= tc), enumerated u -> (ti, tc)
+    const int nlow = nt8 * (nt8 + 1) / 2;
+    auto tile_of = [&](int u, int& ti, int& tc) {
+      ti = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+      while ((ti + 1) * (ti + 2) / 2 <= u) ++ti;
+      while (ti * (ti + 1) / 2 > u) --ti;
+      tc = u - ti * (ti + 1) / 2;
+    };
+    // A := E - X1 X1^T; X1 lower triangular: (X1 X1^T)_ic needs k < 8 (tc + 1)
+    for (int u = warp; u < nlow; u += 8) {
+      int ti, tc;
+      tile_of(u, ti, tc);
+      double m2[2] = {0.0, 0.0}, m3[2] = {0.0, 0.0};
+      const int kend = (tc + 1) * 2;  // k-steps of 4 covering columns < 8 (tc + 1)
+      int ks = 0;
+      for (; ks + 1 < kend; ks += 2) {
         dmma(m2, W[(ti * 8 + g) * ld + ks * 4 + t], W[(tc * 8 + g) * ld + ks * 4 + t]);
-      A[(ti * 8 + g) * ld + tc * 8 + 2 * t] -= m2[0];
-      A[(ti * 8 + g) * ld + tc * 8 + 2 * t + 1] -= m2[1];
+        dmma(m3, W[(ti * 8 + g) * ld + ks * 4 + 4 + t], W[(tc * 8 + g) * ld + ks * 4 + 4 + t]);
+      }
+      if (ks < kend) dmma(m2, W[(ti * 8 + g) * ld + ks * 4 + t], W[(tc * 8 + g) * ld + ks * 4 + t]);
+      A[(ti * 8 + g) * ld + tc * 8 + 2 * t] -= m2[0] + m3[0];
+      A[(ti * 8 + g) * ld + tc * 8 + 2 * t + 1] -= m2[1] + m3[1];
     }
     __syncthreads();
     // W := X = Phi(A)
@@ -679,18 +692,26 @@ __global__ void __launch_bounds__(256) k_chol_b16(const double* __restrict__ gra
       W[i * ld + c] = (c < i) ? A[i * ld + c] : (c == i ? 0.5 * A[i * ld + c] : 0.0);
     }
     __syncthreads();
-    // A := L^-1 = I - X + X^2 (lower tiles; X lower triangular)
+    // A := L^-1 = I - X + X^2; X lower triangular: (X^2)_ic needs
+    // 8 tc <= k < 8 (ti + 1); upper tiles are zero
     for (int u = warp; u < nt8 * nt8; u += 8) {
       const int ti = u / nt8, tc = u % nt8;
-      double m2[2] = {0.0, 0.0};
-      if (tc <= ti)
-        for (int ks = 0; ks < kp / 4; ++ks)
+      double m2[2] = {0.0, 0.0}, m3[2] = {0.0, 0.0};
+      if (tc <= ti) {
+        const int kb = tc * 2, kend = (ti + 1) * 2;
+        int ks = kb;
+        for (; ks + 1 < kend; ks += 2) {
           dmma(m2, W[(ti * 8 + g) * ld + ks * 4 + t], W[(ks * 4 + t) * ld + tc * 8 + g]);
+          dmma(m3, W[(ti * 8 + g) * ld + ks * 4 + 4 + t], W[(ks * 4 + 4 + t) * ld + tc * 8 + g]);
+        }
+        if (ks < kend) dmma(m2, W[(ti * 8 + g) * ld + ks * 4 + t], W[(ks * 4 + t) * ld + tc * 8 + g]);
+      }
       const int i = ti * 8 + g, c0 = tc * 8 + 2 * t;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = c0 + h;
-        A[i * ld + c] = (c <= i) ? ((i == c ? 1.0 : 0.0) - W[i * ld + c] + m2[h]) : 0.0;
+        A[i * ld + c] =
+            (c <= i) ? ((i == c ? 1.0 : 0.0) - W[i * ld + c] + (m2[h] + m3[h])) : 0.0;
       }
     }
     __syncthreads();

@@ -45,22 +45,36 @@ __global__ void lat(double* out, long long* cyc, double x0, int n) {
   t0 = clock64();
   for (int i = 0; i < n; ++i) __syncthreads();
   t1 = clock64(); cyc[7] = t1 - t0;
-  out[0] = x + y + z + w + r + f + idx;
+  // DMMA m8n8k4 f64 dependent chain (same accumulator)
+  double c0 = x0, c1 = x0;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i)
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1) : "d"(0.5), "d"(1e-9));
+  t1 = clock64(); cyc[8] = t1 - t0;
+  // double shuffle chain
+  double sh = x0;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) sh = __shfl_sync(0xffffffffu, sh, (threadIdx.x + 1) & 31) + 1e-9;
+  t1 = clock64(); cyc[9] = t1 - t0;
+  out[0] = x + y + z + w + r + f + idx + c0 + c1 + sh;
 }
 
 int main() {
   double* out; long long* cyc;
-  cudaMalloc(&out, 8); cudaMalloc(&cyc, 8 * 8);
+  cudaMalloc(&out, 8); cudaMalloc(&cyc, 8 * 10);
   const int n = 1000;
   for (int threads : {32, 256}) {
     lat<<<1, threads>>>(out, cyc, 0.5, n);
     lat<<<1, threads>>>(out, cyc, 0.5, n);
     cudaDeviceSynchronize();
-    long long h[8];
+    long long h[10];
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
-    const char* names[8] = {"DFMA", "DADD", "1/x (double div)", "sqrt(double)", "rsqrt(double)", "FFMA", "LDS chain", "__syncthreads"};
+    const char* names[10] = {"DFMA", "DADD", "1/x (double div)", "sqrt(double)", "rsqrt(double)",
+                             "FFMA", "LDS chain", "__syncthreads", "DMMA m8n8k4 chain",
+                             "SHFL double + DADD"};
     printf("threads=%d\n", threads);
-    for (int i = 0; i < 8; ++i) printf("  %-18s %7.1f cycles/op\n", names[i], (double)h[i] / n);
+    for (int i = 0; i < 10; ++i) printf("  %-18s %7.1f cycles/op\n", names[i], (double)h[i] / n);
   }
   // empty kernel launch rate
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
