@@ -212,6 +212,42 @@ int rgsv_svd_values(const double* a, int64_t lda, int rows, int cols, double* sv
  * chol_inv: Cholesky of a k x k Gram (ld kp) [+ shift for `shift_rows`
  *           rows], Linv = L^{-1}, Rinv = Linv^T (kp x kp, identity pad).
  * sumsq   : out[0] = sum of squares of a rows x cols block. */
+/* --- fp32-resident pairs (cfg4): 3xTF32 tcgen05 GEMM passes ------------
+ * The reference promotes fp32 input to fp64 up front (core.py:51-54); these
+ * entry points instead run the G passes of the fixed-rank chain
+ * (rangefinder.py:115, the q power steps, engine.py:255-256) on the
+ * tensor cores in kind::tf32 with a hi/lo operand split (fp32-level
+ * products, fp32 accumulation, fp64 outputs). Matrices are row-major fp32
+ * with ld a multiple of 4 elements and 16-byte aligned bases.
+ *
+ * rgsv_f32_split: lo = tf32(g - hi(g)) for the big operand (hi(g) = g as the
+ * tensor core reads it; mode 0 = low 13 mantissa bits dropped, 1 = nearest)
+ * and, if sumsq_out != NULL, ||g||_F^2 in fp64 (core.sum_sq, core.py:115-125).
+ * ws: >= 1184 doubles of scratch. */
+int rgsv_f32_split(const float* g, int64_t ldg, int64_t rows, int64_t cols, float* lo,
+                   int64_t ldl, int mode, double* sumsq_out, void* ws, size_t ws_bytes,
+                   void* stream);
+/* hi = tf32(x), lo = tf32(x - hi) of an fp64 matrix (rows x cols, ld ldx)
+ * into rows x cols_out fp32 arrays (ld ldo), zero in columns >= cols. */
+int rgsv_f64_split_tf32(const double* x, int64_t ldx, int64_t rows, int64_t cols, float* hi,
+                        float* lo, int64_t ldo, int64_t cols_out, void* stream);
+/* Y (M x N, fp64, ld ldy) = G (M x K) X^T, X given as hi/lo (N x K, ld ldx);
+ * 32 <= N <= 320, N % 32 == 0. */
+int rgsv_tf32x3_gx(const float* g, const float* glo, int64_t ldg, const float* xhi,
+                   const float* xlo, int64_t ldx, double* y, int64_t ldy, int64_t M, int64_t N,
+                   int64_t K, void* stream);
+/* C (N x M, fp64, ld ldc) = Q^T G with Q (K x N, hi/lo, ld ldq) and G
+ * (K x M, + lo, ld ldg); 32 <= N <= 320, N % 32 == 0. The K reduction is
+ * split over CTAs into fp64 partials in `scratch` (RGSV_ERR_WORKSPACE if
+ * too small) and summed in a fixed order. */
+int rgsv_tf32x3_gtq(const float* qhi, const float* qlo, int64_t ldq, const float* g,
+                    const float* glo, int64_t ldg, double* c, int64_t ldc, int64_t N, int64_t M,
+                    int64_t K, void* scratch, size_t scratch_bytes, void* stream);
+/* Tuning knobs: K-block of the two kernels (16 or 32; gtq also 8), rows per
+ * split of the gtq reduction and K-blocks accumulated in TMEM between fp32
+ * register flushes (values out of range are ignored). */
+int rgsv_tf32_config(int bk_gx, int bk_gtq, int rows_per_split, int flush);
+
 int rgsv_gemm_gx(const double* a, int64_t lda, const double* bt, int64_t ldb, double* c,
                  int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
                  size_t scratch_bytes, void* stream);

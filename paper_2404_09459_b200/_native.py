@@ -76,6 +76,12 @@ SIGNATURES = {
     "rgsv_debug_householder_profile": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _p, _i64, _p, _p]),
     "rgsv_debug_chol_profile": (_i32, [_p, _i32, _i32, _p, _p, _p, _p]),
     "rgsv_sumsq": (_i32, [_p, _i64, _i64, _i64, _p, _p, _sz, _p]),
+    "rgsv_f32_split": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _i32, _p, _p, _sz, _p]),
+    "rgsv_f64_split_tf32": (_i32, [_p, _i64, _i64, _i64, _p, _p, _i64, _i64, _p]),
+    "rgsv_tf32x3_gx": (_i32, [_p, _p, _i64, _p, _p, _i64, _p, _i64, _i64, _i64, _i64, _p]),
+    "rgsv_tf32x3_gtq": (_i32, [_p, _p, _i64, _p, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _sz,
+                               _p]),
+    "rgsv_tf32_config": (_i32, [_i32, _i32, _i32, _i32]),
 }
 
 _LIB = None

@@ -65,6 +65,13 @@ static PFN_encodeTiled_t encode_fn() {
 
 int make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer,
                  uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer, int elem_bytes) {
+  return make_tmap_2d_swz(out, base, inner, outer, ld_elems, box_inner, box_outer, elem_bytes,
+                          128);
+}
+
+int make_tmap_2d_swz(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer, int elem_bytes,
+                     int swizzle_bytes) {
   PFN_encodeTiled_t fn = encode_fn();
   if (!fn) return RGSV_ERR_CUDA;
   if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld_elems * elem_bytes) & 15))
@@ -75,7 +82,12 @@ int make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t ou
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(out, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                   2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle_bytes == -128 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                  : swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                  : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                  : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                        : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : RGSV_ERR_CUDA;
 }

@@ -94,5 +94,10 @@ void note_launch(int n = 1);
 // box of box_inner x box_outer elements and 128-byte swizzle.
 int make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer,
                  uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer, int elem_bytes);
+// Same with an explicit swizzle span (128, 64, 32 or 0 bytes; -128 = 128-byte
+// span with 32-byte atoms, the MN-major tf32 operand layout of tcgen05).
+int make_tmap_2d_swz(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer, int elem_bytes,
+                     int swizzle_bytes);
 
 }  // namespace rgsv

@@ -15,8 +15,10 @@ from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
+import torch
 
 from . import device as _dev
+from . import tf32 as _tf32
 from ._native import ST_CHOL, ST_CLASSIFY, ST_JACOBI, ST_OMEGA_SHORT
 from .errors import (
     ConvergenceError,
@@ -161,8 +163,16 @@ class GsvOptions:
     extraction: ExtractionConfig = ExtractionConfig()
     classify_tol: float = 1e-10
     method: str = RANDOMIZED
+    # fp32-resident pairs (not in the reference, which promotes fp32 to fp64
+    # up front, core.py:51-54): "tf32x3" runs the G passes on the tcgen05
+    # tensor cores at fp32-level accuracy (tf32.py); "promote" streams
+    # fp64-promoted row chunks through the DMMA chain (the reference's exact
+    # arithmetic).
+    f32_mode: str = "tf32x3"
 
     def __post_init__(self):
+        if self.f32_mode not in ("tf32x3", "promote"):
+            raise ValidationError(f"f32_mode must be 'tf32x3' or 'promote', got {self.f32_mode!r}")
         if not 0 < self.classify_tol < 1e-2:
             raise ValidationError(f"classify_tol must be in (0, 1e-2), got {self.classify_tol}")
         if self.method not in (RANDOMIZED, DIRECT):
@@ -309,8 +319,20 @@ def _streamed_run(pair: GmpPair, opts: GsvOptions, k1: int, k2: int) -> DeviceRu
     G in fp64-promoted row chunks (rangefinder.chunked_chain), then the
     shared small-GSVD + comparative stage."""
     cfg = opts.extraction
-    _, b1, h1 = chunked_chain(pair.g1, k1, cfg.power_iters, cfg.seed)
-    _, b2, h2 = chunked_chain(pair.g2, k2, cfg.power_iters, cfg.seed + 1)
+    lo = None
+    res = []
+    for g, k, seed in ((pair.g1, k1, cfg.seed), (pair.g2, k2, cfg.seed + 1)):
+        if opts.f32_mode == "tf32x3" and _tf32.supported(g, k):
+            # one fp32 lo buffer (rows x ld) shared by the two chains
+            if lo is None or lo.numel() < g.rows * g.ld:
+                lo = torch.empty(max(pair.g1.rows * pair.g1.ld, pair.g2.rows * pair.g2.ld),
+                                 dtype=torch.float32, device="cuda")
+            buf = lo[: g.rows * g.ld].view(g.rows, g.ld)
+            res.append(_tf32.tf32_chain(g, k, cfg.power_iters, seed, lo=buf))
+        else:
+            res.append(chunked_chain(g, k, cfg.power_iters, seed))
+    (_, b1, h1), (_, b2, h2) = res
+    del lo
     out = _small_checked(b1, k1, b2, k2, pair.n, opts.classify_tol)
     r, s = out["counts"]
     spec = GsvSpectrum(out["alphas"], out["betas"], r, s)

@@ -1,0 +1,145 @@
+"""fp32-resident pairs on the 5th-gen tensor cores (the cfg4 family).
+
+The G passes of the fixed-rank chain -- sketch Y = G Omega
+(rangefinder.py:115), the q power steps Z = G^T Q / Y = G Qhat, and the
+projection B = Q^T G (engine.py:255-256) -- run as tcgen05 kind::tf32 GEMMs
+with a 3xTF32 hi/lo operand split (csrc/tf32x3.cu): fp32-level products at
+three TF32 MMAs each, fp32 accumulation in TMEM, fp64 outputs. The small
+factorizations (shifted CholeskyQR3 of Y and Z, the stacked QR, Jacobi and
+the comparative kernel) stay fp64 on the DMMA path.
+
+The reference promotes fp32 input to fp64 up front (core.py:51-54); the
+promoted chain (rangefinder.chunked_chain) reproduces that exactly and stays
+available as GsvOptions(f32_mode="promote"). This module is the fp32
+compute path BASELINE.json's cfg4 asks for (tolerance 1e-4 on the GSVs and
+theta); tests/test_gpu_tf32.py pins it against the fp64 oracle.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import device as _dev
+from ._native import check, lib
+from .errors import RankDeficiencyError, ValidationError
+
+F32, F64 = torch.float32, torch.float64
+ST_CHOL = 0x1
+
+# How the tensor core reads the low 13 mantissa bits of a raw fp32 operand
+# (0: dropped, 1: rounded to nearest); lo = tf32(g - hi(g)) must use the same
+# hi. Measured on B200 by tests/test_gpu_tf32.py::test_tc_reads_fp32_as.
+HI_MODE = 0
+
+
+def _ceil(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+class TF32Ops:
+    """Launch helpers on the current stream (scratch owned here)."""
+
+    def __init__(self):
+        self.L = lib()
+        self.scratch = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+        self.ws = torch.empty(4096, dtype=F64, device="cuda")
+
+    @staticmethod
+    def st():
+        return _dev.sp(torch.cuda.current_stream())
+
+    def split_big(self, g: "_dev.DevMatrix", lo: torch.Tensor | None = None):
+        """(lo, ||G||_F^2 as a device scalar) for an fp32 DevMatrix."""
+        if lo is None:
+            lo = torch.empty((g.rows, g.ld), dtype=F32, device="cuda")
+        ss = torch.zeros(1, dtype=F64, device="cuda")
+        check(self.L.rgsv_f32_split(_dev.vp(g.t), g.ld, g.rows, g.cols, _dev.vp(lo), lo.stride(0),
+                                    HI_MODE, _dev.vp(ss), _dev.vp(self.ws), self.ws.numel() * 8,
+                                    self.st()), "f32_split")
+        return lo, ss
+
+    def split_small(self, x: torch.Tensor, rows: int, cols: int, cols_out: int,
+                    rows_out: int | None = None):
+        """hi/lo fp32 (rows_out x cols_out, zero padded) of an fp64 matrix x
+        (rows x cols)."""
+        ro = rows_out or rows
+        alloc = torch.zeros if ro > rows else torch.empty
+        hi = alloc((ro, cols_out), dtype=F32, device="cuda")
+        lo = alloc((ro, cols_out), dtype=F32, device="cuda")
+        check(self.L.rgsv_f64_split_tf32(_dev.vp(x), x.stride(0), rows, cols, _dev.vp(hi),
+                                         _dev.vp(lo), cols_out, cols_out, self.st()),
+              "f64_split_tf32")
+        return hi, lo
+
+    def gx(self, g, glo, xhi, xlo, y, M: int, N: int, K: int):
+        """y (M x N fp64) = G (M x K) X^T."""
+        check(self.L.rgsv_tf32x3_gx(_dev.vp(g.t), _dev.vp(glo), g.ld, _dev.vp(xhi), _dev.vp(xlo),
+                                    xhi.stride(0), _dev.vp(y), y.stride(0), M, N, K, self.st()),
+              "tf32x3_gx")
+
+    def gtq(self, qhi, qlo, g, glo, out, N: int, M: int, K: int):
+        """out (N x M fp64) = Q^T G (split-K partials in scratch, grown on demand)."""
+        while True:
+            rc = self.L.rgsv_tf32x3_gtq(_dev.vp(qhi), _dev.vp(qlo), qhi.stride(0), _dev.vp(g.t),
+                                        _dev.vp(glo), g.ld, _dev.vp(out), out.stride(0), N, M, K,
+                                        _dev.vp(self.scratch), self.scratch.numel(), self.st())
+            if rc != 6:  # RGSV_ERR_WORKSPACE
+                return check(rc, "tf32x3_gtq")
+            self.scratch = torch.empty(self.scratch.numel() * 4, dtype=torch.uint8, device="cuda")
+
+
+def supported(g: "_dev.DevMatrix", k: int) -> bool:
+    """Shapes served by the tf32x3 kernels (else the promoted fp64 chain)."""
+    kq = _ceil(_dev.ceil16(k), 32)
+    return g.is_f32 and g.ld % 4 == 0 and g.t.data_ptr() % 16 == 0 and kq <= 320 and \
+        g.cols >= 1 and g.rows >= 1
+
+
+def tf32_chain(a: "_dev.DevMatrix", k: int, q: int, seed: int, lo: torch.Tensor | None = None):
+    """Fixed-rank chain (sketch, shifted CholeskyQR3, q power iterations,
+    projection; rangefinder.py:115-123 + SURVEY.md §8(c)) with the four G
+    passes on the tf32x3 tensor-core kernels. Returns (Q: m x kp fp64,
+    B = Q^T G: kp x ldn fp64, residual history). `lo` may pass a reusable
+    (rows x ld) fp32 buffer for G's low part."""
+    from .rangefinder import _Ops
+
+    ops = _Ops()
+    t = TF32Ops()
+    m, n = a.rows, a.cols
+    if k > min(m, n):
+        raise ValidationError(f"max_cols={k} exceeds min(rows, cols)={min(m, n)}")
+    kp, ldn = _dev.ceil16(k), _dev.ceil16(n)
+    kq = _ceil(kp, 32)
+    glo, ss = t.split_big(a, lo)
+    om = _dev.omega_device(n, k, [seed], ldo=ldn)[0]
+    ops.status.zero_()
+
+    def pass_gx(xt):
+        xh, xl = t.split_small(xt, kp, ldn, ldn, rows_out=kq)
+        y = torch.empty((m, kq), dtype=F64, device="cuda")
+        t.gx(a, glo, xh, xl, y, m, kq, n)
+        return y if kq == kp else y[:, :kp].contiguous()
+
+    def pass_gtq(qm):
+        qh, ql = t.split_small(qm, m, kp, kq)
+        out = torch.zeros((kq, ldn), dtype=F64, device="cuda")
+        t.gtq(qh, ql, a, glo, out, kq, n, m)
+        return out[:kp]
+
+    y = pass_gx(om)
+    gf2 = float(ss.item())
+    if not math.isfinite(gf2):
+        raise ValidationError("g contains non-finite entries")
+    qm = ops.cholqr3(y, m, k, kp)
+    for _ in range(q):
+        zt = pass_gtq(qm)
+        qht = ops.wide_cholqr3(zt.contiguous(), n, ldn, k, kp)
+        y = pass_gx(qht)
+        qm = ops.cholqr3(y, m, k, kp)
+    b = pass_gtq(qm).contiguous()
+    energy = ops.sumsq(_dev.vp(b), ldn, k, n)
+    if int(ops.status.item()) & ST_CHOL:
+        raise RankDeficiencyError("CholeskyQR breakdown in the range finder (rank-deficient sketch)")
+    return qm, b, _dev.residual_history(gf2, energy)

@@ -56,7 +56,7 @@ def test_chunked_chain_matches_oracle(rg, chunk_rows):
 
 def test_f32_pair_compare_matches_f64(rg):
     g1, g2 = _f32_pair()
-    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(24, 5, 1))
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(24, 5, 1), f32_mode="promote")
     r32 = rg.compare(rg.GmpPair(g1, g2), opts)
     r64 = rg.compare(rg.GmpPair(g1.astype(np.float64), g2.astype(np.float64)), opts)
     assert np.array_equal(r32.spectrum.alphas, r64.spectrum.alphas)
