@@ -14,6 +14,9 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "rgsv_internal.h"
 
@@ -852,6 +855,192 @@ __global__ void __launch_bounds__(256) k_chol_b16(const double* __restrict__ gra
   }
 }
 
+// ------------------------------------------- blocked, 128 < kp <= 1024
+// kp beyond one CTA's shared memory (cfg4: the 288-wide range-finder blocks
+// and the 576-wide stacked pair). Right-looking blocked Cholesky on a global
+// (L2-resident) working copy: each <= 128-wide diagonal block is factorised
+// by k_chol_blk (which also returns its inverse), panels and trailing
+// updates are DMMA GEMMs, and L^{-1} is assembled block by block
+// (X_IJ = -L_II^{-1} sum_{J<=K<I} L_IK X_KJ). Same outputs and identity
+// padding as the one-CTA kernels.
+
+// W = gram (+ shift s I on the k real columns, identity on the padding);
+// every block recomputes the trace (k <= 1024 diagonal reads).
+__global__ void k_chol_prep(const double* __restrict__ gram, int k, int kp, int64_t shift_rows,
+                            double* __restrict__ W) {
+  double sh = 0.0;
+  if (shift_rows > 0) {
+    double tr = 0.0;
+    for (int i = 0; i < k; ++i) tr += gram[(int64_t)i * kp + i];
+    sh = 11.0 * ((double)shift_rows * k + (double)k * (k + 1)) * 0x1p-53 * tr;
+  }
+  const int64_t total = (int64_t)kp * kp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / kp), j = (int)(e % kp);
+    double v;
+    if (i < k && j < k)
+      v = gram[e] + (i == j ? sh : 0.0);
+    else
+      v = (i == j) ? 1.0 : 0.0;
+    W[e] = v;
+  }
+}
+
+// linv = X (lower part), rinv = X^T.
+__global__ void k_chol_finish(const double* __restrict__ X, int kp, double* __restrict__ linv,
+                              double* __restrict__ rinv) {
+  const int64_t total = (int64_t)kp * kp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / kp), j = (int)(e % kp);
+    const double x = (j <= i) ? X[e] : 0.0;
+    linv[e] = x;
+    if (rinv) rinv[(int64_t)j * kp + i] = x;
+  }
+}
+
+__global__ void k_identity2(double* __restrict__ a, double* __restrict__ b, int n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const double v = (e / n == e % n) ? 1.0 : 0.0;
+    a[e] = v;
+    b[e] = v;
+  }
+}
+
+namespace {
+
+struct BlkScratch {
+  double* base = nullptr;
+  size_t bytes = 0;
+};
+
+// One scratch area per stream (kp <= 1024 needs ~4 kp^2 + 10 * 128^2 doubles).
+double* blk_scratch(cudaStream_t st, size_t need) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, BlkScratch> pool;
+  std::lock_guard<std::mutex> lock(mu);
+  BlkScratch& b = pool[st];
+  if (b.bytes < need) {
+    if (b.base) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.base);
+    }
+    b.base = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.base, need) != cudaSuccess) return nullptr;
+    b.bytes = need;
+  }
+  return b.base;
+}
+
+int gemm_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+               int64_t M, int64_t N, int64_t K, bool gtq, cudaStream_t st) {
+  GemmArgs g;
+  g.A = A;
+  g.lda = lda;
+  g.B = B;
+  g.ldb = ldb;
+  g.C = C;
+  g.ldc = ldc;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.max_split = 1;
+  return gtq ? gemm_gtq(g, st) : gemm_gx(g, st);
+}
+
+int copy2d(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
+           cudaStream_t st) {
+  return cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double),
+                           cols * sizeof(double), rows, cudaMemcpyDeviceToDevice, st) == cudaSuccess
+             ? 0
+             : RGSV_ERR_CUDA;
+}
+
+}  // namespace
+
+int launch_axpy(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols,
+                double alpha, cudaStream_t st);
+int launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
+                      int transpose, cudaStream_t st);
+
+int chol_inv_blocked(const double* gram, int k, int kp, int64_t shift_rows, double* linv,
+                     double* rinv, double* r_upper, double* rdiag, double* rdiag_acc, int* status,
+                     cudaStream_t st) {
+  if (r_upper) return RGSV_ERR_DIMENSION;  // R = L^T is only requested for kp <= 128
+  const int nb = (kp + 127) / 128;
+  const int bs = ((kp + nb - 1) / nb + 15) / 16 * 16;  // block size, multiple of 16, <= 128
+  const size_t kk = (size_t)kp * kp, bb = (size_t)128 * 128;
+  double* base = blk_scratch(st, (4 * kk + (4 + (size_t)nb) * bb + 8 * 128) * sizeof(double));
+  if (!base) return RGSV_ERR_CUDA;
+  double* W = base;            // working copy; lower part becomes L
+  double* X = W + kk;          // L^{-1}
+  double* T = X + kk;          // GEMM outputs (<= kp x kp)
+  double* T2 = T + kk;
+  double* D = T2 + kk;         // diagonal block input (bs x bs)
+  double* DL = D + bb;         // its L^{-1} (k_chol_blk output, + work)
+  double* RI = DL + 2 * bb;    // per block: L_II^{-T} (bs x bs each)
+  if (cudaMemsetAsync(X, 0, kk * sizeof(double), st) != cudaSuccess) return RGSV_ERR_CUDA;
+  k_chol_prep<<<64, 256, 0, st>>>(gram, k, kp, shift_rows, W);
+  note_launch();
+  for (int J = 0; J < nb; ++J) {
+    const int o = J * bs;
+    if (o >= kp) break;
+    const int s = kp - o < bs ? kp - o : bs;
+    const int kr = k - o < 0 ? 0 : (k - o < s ? k - o : s);
+    const int below = kp - o - s;
+    // (a) diagonal block: L_JJ^{-1} (and its transpose) by the one-CTA kernel
+    if (int e = copy2d(D, s, W + (size_t)o * kp + o, kp, s, s, st)) return e;
+    double* rij = RI + (size_t)J * bb;
+    if (kr > 0) {
+      if (int e = chol_inv(D, kr, s, 0, DL, rij, nullptr, rdiag ? rdiag + o : nullptr,
+                           rdiag_acc ? rdiag_acc + o : nullptr, status, st))
+        return e;
+    } else {  // pure padding: identity
+      k_identity2<<<8, 256, 0, st>>>(DL, rij, s);
+      note_launch();
+    }
+    if (int e = copy2d(X + (size_t)o * kp + o, kp, DL, s, s, s, st)) return e;
+    if (below > 0) {
+      // (b) panel L_{>J,J} = A_{>J,J} L_JJ^{-T}
+      double* P = W + (size_t)(o + s) * kp + o;
+      if (int e = gemm_small(P, kp, DL, s, T, s, below, s, s, false, st)) return e;
+      if (int e = copy2d(P, kp, T, s, below, s, st)) return e;
+      // (c) trailing A_{>J,>J} -= L_{>J,J} L_{>J,J}^T
+      if (int e = gemm_small(P, kp, P, kp, T2, below, below, below, s, false, st)) return e;
+      if (int e = launch_axpy(W + (size_t)(o + s) * kp + o + s, kp, T2, below, below, below, -1.0,
+                              st))
+        return e;
+    }
+  }
+  // (d) X_IJ = -L_II^{-1} sum_{J<=K<I} L_IK X_KJ, block column by block column
+  for (int J = 0; J < nb; ++J) {
+    const int oj = J * bs;
+    if (oj >= kp) break;
+    const int sj = kp - oj < bs ? kp - oj : bs;
+    for (int I = J + 1; I < nb; ++I) {
+      const int oi = I * bs;
+      if (oi >= kp) break;
+      const int si = kp - oi < bs ? kp - oi : bs;
+      // S (si x sj) = L[oi:oi+si, oj:oi] X[oj:oi, oj:oj+sj] as gx (A Bt^T) with
+      // Bt = X[oj:oi, J]^T, transposed into T2 (sj x kk2)
+      const int kk2 = oi - oj;
+      if (int e = launch_copy_block(T2, kk2, X + (size_t)oj * kp + oj, kp, sj, kk2, 1, st))
+        return e;
+      if (int e = gemm_small(W + (size_t)oi * kp + oj, kp, T2, kk2, T, sj, si, sj, kk2, false, st))
+        return e;
+      // X_IJ = -L_II^{-1} S: gtq(A = L_II^{-T} (si x si), B = S) = L_II^{-1} S
+      if (int e = gemm_small(RI + (size_t)I * bb, si, T, sj, T2, sj, si, sj, si, true, st))
+        return e;
+      if (int e = launch_axpy(X + (size_t)oi * kp + oj, kp, T2, sj, si, sj, -1.0, st)) return e;
+    }
+  }
+  k_chol_finish<<<64, 256, 0, st>>>(X, kp, linv, rinv);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
+}
+
 int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
              double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st) {
   if (k <= 0 || kp < k || kp % 16 != 0 || kp > 1024) return RGSV_ERR_DIMENSION;
@@ -890,6 +1079,10 @@ int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
   }
+  static const bool unblocked = getenv("RGSV_CHOL_UNBLOCKED") != nullptr;
+  if (!unblocked && !r_upper)
+    return chol_inv_blocked(gram, k, kp, shift_rows, linv, rinv, r_upper, rdiag, rdiag_acc, status,
+                            st);
   const size_t wbytes = (size_t)kp * (kp + 1) * sizeof(double);
   if (wbytes <= 200 * 1024) {
     static bool attr = false;

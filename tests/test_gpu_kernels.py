@@ -89,7 +89,7 @@ def test_gemm_deterministic():
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("k", [1, 5, 16, 60, 64, 120, 240])
+@pytest.mark.parametrize("k", [1, 5, 16, 60, 64, 120, 129, 240, 288, 300, 576, 700])
 def test_chol_inv(k):
     kp = (k + 15) // 16 * 16
     rng = np.random.default_rng(k)
@@ -113,8 +113,9 @@ def test_chol_inv(k):
     assert relerr(rd[:k].cpu().numpy(), np.diag(L)) <= 1e-13
 
 
-def test_chol_breakdown_flag():
-    k = kp = 16
+@pytest.mark.parametrize("k", [16, 288])
+def test_chol_breakdown_flag(k):
+    kp = k
     G = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")  # singular
     linv = torch.zeros(kp * kp + kp * (kp + 1), dtype=torch.float64, device="cuda")
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
