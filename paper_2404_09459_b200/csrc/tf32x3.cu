@@ -414,10 +414,14 @@ int first_chunk(int N) {
   return (N / 2 + 31) / 32 * 32;
 }
 
-int g_bk_gx = 16;   // K-block (16: 64B swizzle rows, 32: 128B) of the gx kernel
-int g_bk_gtq = 16;  // K-block (rows) of the gtq kernel
+// Tuned on B200 at cfg4 shapes (tools/tf32_sweep.py, m = 1e6, n = 8192, N = 288):
+// gx / gtq at BK 16, flush 1: 126 / 108 TFLOP/s; BK 32, flush 2: 160 / 159.
+// A flush every 2 K-blocks keeps 64 K-steps (24 MMAs) in the truncating TMEM
+// accumulator: relative error ~5e-7, the level of an fp32 SGEMM.
+int g_bk_gx = 32;   // K-block (16: 64B swizzle rows, 32: 128B) of the gx kernel
+int g_bk_gtq = 32;  // K-block (rows) of the gtq kernel
 int g_rows_per_split = 8192;
-int g_flush = 1;    // K-blocks accumulated in TMEM before an fp32 register flush
+int g_flush = 2;    // K-blocks accumulated in TMEM before an fp32 register flush
 
 template <int MODE, int BK>
 int launch_bk(const CUtensorMap& tg, const CUtensorMap& tgl, const CUtensorMap& tbh,

@@ -106,7 +106,7 @@ def test_gtq_accuracy(rg, K, M, N, rows_per):
         t.gtq(qh, ql, g, lo, out2, N, M, K)
         assert torch.equal(out[:, :M], out2[:, :M])
     finally:
-        L.rgsv_tf32_config(0, 0, 8192, 0)
+        L.rgsv_tf32_config(0, 0, 8192, 0)  # restore the default split
 
 
 def _f32_pair(m=3000, p=2400, n=300, seed=11):
