@@ -97,6 +97,51 @@ def supported(g: "_dev.DevMatrix", k: int) -> bool:
         g.cols >= 1 and g.rows >= 1
 
 
+def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, final: bool):
+    """Shifted CholeskyQR for the fp32 chain (m x kp fp64 Y -> Q, zero padded).
+
+    Pass 1: fp64 Gram (shifted) and Cholesky -- the Gram's condition is
+    cond(Y)^2, beyond fp32 -- with the TRSM Y L^-T on the tensor cores
+    (3xTF32). Pass 2: 3xTF32 Gram and TRSM of the now well-conditioned Q1.
+    Pass 3 (final basis only): fp64 Gram, Cholesky and TRSM, so the returned
+    Q is orthonormal to fp64 precision. Every factor is triangular, so the
+    nested leading spans are those of Y (the intermediate basis of a power
+    step only needs its span: two passes)."""
+    kq = _ceil(kp, 32)
+    f64 = torch.float64
+
+    def trsm_tc(src_hi, src_lo, linv):
+        xh, xl = t.split_small(linv, kp, kp, kp, rows_out=kq)
+        out = torch.empty((m, kq), dtype=f64, device="cuda")
+        t.gx(_dev.DevMatrix(src_hi[:, :kp], m, kp), src_lo, xh, xl, out, m, kq, kp)
+        return out
+
+    # pass 1
+    gram = torch.zeros((kp, kp), dtype=f64, device="cuda")
+    ops.gtq(_dev.vp(y), kp, _dev.vp(y), kp, _dev.vp(gram), kp, kp, kp, m)
+    linv, _ = ops.chol(gram, k, kp, m)
+    yh, yl = t.split_small(y, m, kp, kp)
+    q1 = trsm_tc(yh, yl, linv)
+    del yh, yl
+    # pass 2
+    qh, ql = t.split_small(q1, m, kp, kq)
+    g2 = torch.zeros((kq, kq), dtype=f64, device="cuda")
+    t.gtq(qh, ql, _dev.DevMatrix(qh[:, :kp], m, kp), ql, g2, kq, kp, m)
+    linv2, _ = ops.chol(g2[:kp, :kp].contiguous(), k, kp, 0)
+    q2 = trsm_tc(qh, ql, linv2)
+    del qh, ql, q1
+    q2 = q2 if kq == kp else q2[:, :kp].contiguous()
+    if not final:
+        return q2
+    # pass 3 (fp64)
+    gram3 = torch.zeros((kp, kp), dtype=f64, device="cuda")
+    ops.gtq(_dev.vp(q2), kp, _dev.vp(q2), kp, _dev.vp(gram3), kp, kp, kp, m)
+    linv3, _ = ops.chol(gram3, k, kp, 0)
+    q = torch.zeros((m, kp), dtype=f64, device="cuda")
+    ops.gx(_dev.vp(q2), kp, _dev.vp(linv3), kp, _dev.vp(q), kp, m, kp, kp)
+    return q
+
+
 def tf32_chain(a: "_dev.DevMatrix", k: int, q: int, seed: int, lo: torch.Tensor | None = None):
     """Fixed-rank chain (sketch, shifted CholeskyQR3, q power iterations,
     projection; rangefinder.py:115-123 + SURVEY.md §8(c)) with the four G
@@ -132,12 +177,12 @@ def tf32_chain(a: "_dev.DevMatrix", k: int, q: int, seed: int, lo: torch.Tensor 
     gf2 = float(ss.item())
     if not math.isfinite(gf2):
         raise ValidationError("g contains non-finite entries")
-    qm = ops.cholqr3(y, m, k, kp)
-    for _ in range(q):
+    qm = cholqr_mixed(ops, t, y, m, k, kp, final=q == 0)
+    for it in range(q):
         zt = pass_gtq(qm)
         qht = ops.wide_cholqr3(zt.contiguous(), n, ldn, k, kp)
         y = pass_gx(qht)
-        qm = ops.cholqr3(y, m, k, kp)
+        qm = cholqr_mixed(ops, t, y, m, k, kp, final=it == q - 1)
     b = pass_gtq(qm).contiguous()
     energy = ops.sumsq(_dev.vp(b), ldn, k, n)
     if int(ops.status.item()) & ST_CHOL:

