@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="ONE pair row-sharded over the ranks (dist.compute_gsv_sharded, NCCL "
+                         "all-reduce of the Gram / Z / B partials): strong scaling, cfg2/cfg4")
     return ap.parse_args()
 
 
@@ -519,6 +522,104 @@ def run_ours_f32(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+def device_matrix(rows, cfg, a_seed, bmat, d, dtype):
+    """G = (A diag d) B^T + eps E generated on the device in row chunks."""
+    import torch
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    gen = torch.Generator(device="cuda").manual_seed(a_seed)
+    g = torch.empty((rows, cfg.n), dtype=dtype, device="cuda")
+    R = 1 << 15
+    for r0 in range(0, rows, R):
+        r1 = min(rows, r0 + R)
+        a = torch.randn((r1 - r0, cfg.s), generator=gen, device="cuda", dtype=dtype)
+        g[r0:r1] = (a * d) @ bmat.T
+        g[r0:r1] += cfg.eps * torch.randn((r1 - r0, cfg.n), generator=gen, device="cuda",
+                                          dtype=dtype)
+    return g
+
+
+def run_ours_sharded(args, rank, world):
+    """ONE pair per step, G1/G2 row-sharded over the ranks (genes), every
+    k x k Gram, Z^T and B partial all-reduced with NCCL (dist.py): strong
+    scaling. fp32 configs take the tf32x3 tensor-core chain."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_09459_b200 import _native
+    from paper_2404_09459_b200 import dist as rdist
+    from paper_2404_09459_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    f32 = cfg.dtype == "f32"
+    dt = torch.float32 if f32 else torch.float64
+    gen = torch.Generator(device="cuda").manual_seed(77)  # B shared by all ranks
+    b1 = torch.randn((cfg.n, cfg.s), generator=gen, device="cuda", dtype=dt)
+    b2 = torch.cat([b1[:, : cfg.shared],
+                    torch.randn((cfg.n, cfg.s - cfg.shared), generator=gen, device="cuda",
+                                dtype=dt)], dim=1)
+    d = (10.0 ** (-cfg.decay * torch.arange(cfg.s, device="cuda", dtype=torch.float64)
+                  / cfg.s)).to(dt)
+    r0, r1 = rdist.shard_rows(cfg.m, rank, world)
+    s0, s1 = rdist.shard_rows(cfg.p, rank, world)
+    g1 = device_matrix(r1 - r0, cfg, 1000 + rank, b1, d, dt)
+    g2 = device_matrix(s1 - s0, cfg, 2000 + rank, b2, d, dt)
+
+    def step(i):
+        return rdist.compute_gsv_sharded(g1, g2, cfg.m, cfg.p, cfg.n, cfg.k, cfg.q, seed=i)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
+    l0 = _native.lib().rgsv_launch_count()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        res = step(i)
+    e1.record(stream)
+    barrier()
+    launches = _native.lib().rgsv_launch_count() - l0
+    clk = clocks.stop() if clocks else None
+    tt = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max = float(tt.item())
+    value = args.steps / t_max
+    if rank == 0:
+        peak = MEASURED_BF16_TFLOPS / 6.0 if f32 else FP64_DMMA_PEAK_TFLOPS
+        eff = cfg.flops * value / world / 1e12
+        line = {
+            "metric": f"rGSVD pairs/sec ({cfg.name}, one pair row-sharded over {world} GPU)",
+            "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (3xTF32 tensor cores)" if f32 else "f64",
+            "data": "synthetic (device-generated per rank with the workloads.py recipe)",
+            "config": {"workload": workload_desc(cfg), "g_bytes": cfg.g_bytes,
+                       "parallelism": f"row-sharded x{world} (NCCL all-reduce of Gram/Z/B)",
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "tensor", "kernel": "whole chain (GEMM flops / step time)",
+                         "achieved": eff, "peak": peak, "unit": "TFLOP/s", "frac": eff / peak,
+                         "traffic": None,
+                         "peak_source": "3xTF32 = measured bf16 / 6" if f32 else
+                                        "measured FP64 DMMA issue peak"},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "check": {"r": int(res.r), "s": int(res.s)},
+        }
+        print(json.dumps(line), flush=True)
+
+
 def run_ours(args, rank, world):
     import numpy as np
     import torch
@@ -721,6 +822,8 @@ def main():
 
     if CONFIGS[args.config].batch > 1:
         run_ours_batch(args, rank, world)
+    elif args.sharded:
+        run_ours_sharded(args, rank, world)
     elif CONFIGS[args.config].dtype == "f32":
         run_ours_f32(args, rank, world)
     else:

@@ -194,18 +194,44 @@ def sharded_chain(be, g_local, m_total: int, m_local: int, n: int, k: int, q: in
     return b, gf2, energy
 
 
+def sharded_chain_f32(be, g_local, m_total: int, n: int, k: int, q: int, seed: int, lo=None):
+    """One matrix chain on a row-sharded fp32 G: the tf32x3 tensor-core chain
+    (tf32.tf32_chain) with every k x k Gram, Z^T, B and ||G||^2 partial
+    all-reduced over the ranks."""
+    from . import tf32 as _tf32
+
+    a = _dev.to_device(g_local, "g_local", keep_f32=True)
+    _, b, hist = _tf32.tf32_chain(a, k, q, seed, lo=lo, reduce=_all_reduce, rows_total=m_total)
+    energy = float(be.sumsq(b, b.shape[0], n).cpu()[0])
+    return b, hist[0] ** 2, energy
+
+
+def _is_f32_cuda(t) -> bool:
+    return isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
+
+
 def compute_gsv_sharded(g1_local, g2_local, m: int, p: int, n: int, k: int, q: int = 0,
                         seed: int = 0, classify_tol: float = 1e-10, backend=None):
     """Row-sharded compute_gsv for the fixed-rank pipeline. `g1_local` /
     `g2_local` are this rank's row blocks (see shard_rows). Every rank
-    returns the same ShardedResult."""
+    returns the same ShardedResult. fp32 CUDA shards (cfg4) take the
+    tensor-core tf32x3 chain; fp64 shards the DMMA chain."""
     be = backend or CudaBackend()
     if k > min(m, n) or k > min(p, n):
         raise ValidationError(f"max_cols={k} exceeds min(rows, cols)")
     m_local = g1_local.shape[0]
     p_local = g2_local.shape[0]
-    b1, gf1, e1 = sharded_chain(be, g1_local, m, m_local, n, k, q, seed)
-    b2, gf2, e2 = sharded_chain(be, g2_local, p, p_local, n, k, q, seed + 1)
+    if backend is None and _is_f32_cuda(g1_local) and _is_f32_cuda(g2_local):
+        lo = torch.empty(max(g1_local.numel(), g2_local.numel()), dtype=torch.float32,
+                         device="cuda")
+        b1, gf1, e1 = sharded_chain_f32(be, g1_local, m, n, k, q, seed,
+                                        lo=lo[: g1_local.numel()].view(g1_local.shape))
+        b2, gf2, e2 = sharded_chain_f32(be, g2_local, p, n, k, q, seed + 1,
+                                        lo=lo[: g2_local.numel()].view(g2_local.shape))
+        del lo
+    else:
+        b1, gf1, e1 = sharded_chain(be, g1_local, m, m_local, n, k, q, seed)
+        b2, gf2, e2 = sharded_chain(be, g2_local, p, p_local, n, k, q, seed + 1)
     alphas, betas, r, s, code = be.spectrum(b1, b2, k, k, n, classify_tol)
     if code & ST_OMEGA_SHORT:
         raise RuntimeError("device Omega generator exhausted its draw margin")
@@ -219,4 +245,4 @@ def compute_gsv_sharded(g1_local, g2_local, m: int, p: int, n: int, k: int, q: i
 
 
 __all__ = ["shard_rows", "CudaBackend", "compute_gsv_sharded", "ShardedResult",
-           "sharded_cholqr3", "wide_cholqr3", "sharded_chain"]
+           "sharded_cholqr3", "wide_cholqr3", "sharded_chain", "sharded_chain_f32"]

@@ -97,7 +97,12 @@ def supported(g: "_dev.DevMatrix", k: int) -> bool:
         g.cols >= 1 and g.rows >= 1
 
 
-def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, final: bool):
+def _noreduce(x):
+    return x
+
+
+def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, final: bool,
+                 reduce=_noreduce, rows_total: int | None = None):
     """Shifted CholeskyQR for the fp32 chain (m x kp fp64 Y -> Q, zero padded).
 
     Pass 1: fp64 Gram (shifted) and Cholesky -- the Gram's condition is
@@ -106,7 +111,8 @@ def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, fina
     Pass 3 (final basis only): fp64 Gram, Cholesky and TRSM, so the returned
     Q is orthonormal to fp64 precision. Every factor is triangular, so the
     nested leading spans are those of Y (the intermediate basis of a power
-    step only needs its span: two passes)."""
+    step only needs its span: two passes). For a row-sharded Y (dist.py)
+    `reduce` all-reduces each k x k Gram and `rows_total` sets the shift."""
     kq = _ceil(kp, 32)
     f64 = torch.float64
 
@@ -119,7 +125,7 @@ def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, fina
     # pass 1
     gram = torch.zeros((kp, kp), dtype=f64, device="cuda")
     ops.gtq(_dev.vp(y), kp, _dev.vp(y), kp, _dev.vp(gram), kp, kp, kp, m)
-    linv, _ = ops.chol(gram, k, kp, m)
+    linv, _ = ops.chol(reduce(gram), k, kp, rows_total or m)
     yh, yl = t.split_small(y, m, kp, kp)
     q1 = trsm_tc(yh, yl, linv)
     del yh, yl
@@ -127,7 +133,7 @@ def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, fina
     qh, ql = t.split_small(q1, m, kp, kq)
     g2 = torch.zeros((kq, kq), dtype=f64, device="cuda")
     t.gtq(qh, ql, _dev.DevMatrix(qh[:, :kp], m, kp), ql, g2, kq, kp, m)
-    linv2, _ = ops.chol(g2[:kp, :kp].contiguous(), k, kp, 0)
+    linv2, _ = ops.chol(reduce(g2[:kp, :kp].contiguous()), k, kp, 0)
     q2 = trsm_tc(qh, ql, linv2)
     del qh, ql, q1
     q2 = q2 if kq == kp else q2[:, :kp].contiguous()
@@ -136,28 +142,34 @@ def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, fina
     # pass 3 (fp64)
     gram3 = torch.zeros((kp, kp), dtype=f64, device="cuda")
     ops.gtq(_dev.vp(q2), kp, _dev.vp(q2), kp, _dev.vp(gram3), kp, kp, kp, m)
-    linv3, _ = ops.chol(gram3, k, kp, 0)
+    linv3, _ = ops.chol(reduce(gram3), k, kp, 0)
     q = torch.zeros((m, kp), dtype=f64, device="cuda")
     ops.gx(_dev.vp(q2), kp, _dev.vp(linv3), kp, _dev.vp(q), kp, m, kp, kp)
     return q
 
 
-def tf32_chain(a: "_dev.DevMatrix", k: int, q: int, seed: int, lo: torch.Tensor | None = None):
+def tf32_chain(a: "_dev.DevMatrix", k: int, q: int, seed: int, lo: torch.Tensor | None = None,
+               reduce=_noreduce, rows_total: int | None = None):
     """Fixed-rank chain (sketch, shifted CholeskyQR3, q power iterations,
     projection; rangefinder.py:115-123 + SURVEY.md §8(c)) with the four G
     passes on the tf32x3 tensor-core kernels. Returns (Q: m x kp fp64,
     B = Q^T G: kp x ldn fp64, residual history). `lo` may pass a reusable
-    (rows x ld) fp32 buffer for G's low part."""
+    (rows x ld) fp32 buffer for G's low part. Row-sharded use (dist.py): `a`
+    is this rank's row block, `reduce` all-reduces the k x k Grams, Z^T, B
+    and ||G||^2 partials over the ranks and `rows_total` is the global row
+    count (CholeskyQR shift)."""
     from .rangefinder import _Ops
 
     ops = _Ops()
     t = TF32Ops()
     m, n = a.rows, a.cols
-    if k > min(m, n):
-        raise ValidationError(f"max_cols={k} exceeds min(rows, cols)={min(m, n)}")
+    mt = rows_total or m
+    if k > min(mt, n):
+        raise ValidationError(f"max_cols={k} exceeds min(rows, cols)={min(mt, n)}")
     kp, ldn = _dev.ceil16(k), _dev.ceil16(n)
     kq = _ceil(kp, 32)
     glo, ss = t.split_big(a, lo)
+    reduce(ss)
     om = _dev.omega_device(n, k, [seed], ldo=ldn)[0]
     ops.status.zero_()
 
@@ -171,18 +183,19 @@ def tf32_chain(a: "_dev.DevMatrix", k: int, q: int, seed: int, lo: torch.Tensor 
         qh, ql = t.split_small(qm, m, kp, kq)
         out = torch.zeros((kq, ldn), dtype=F64, device="cuda")
         t.gtq(qh, ql, a, glo, out, kq, n, m)
-        return out[:kp]
+        return reduce(out)[:kp]
 
     y = pass_gx(om)
     gf2 = float(ss.item())
     if not math.isfinite(gf2):
         raise ValidationError("g contains non-finite entries")
-    qm = cholqr_mixed(ops, t, y, m, k, kp, final=q == 0)
+    qm = cholqr_mixed(ops, t, y, m, k, kp, final=q == 0, reduce=reduce, rows_total=mt)
     for it in range(q):
         zt = pass_gtq(qm)
         qht = ops.wide_cholqr3(zt.contiguous(), n, ldn, k, kp)
         y = pass_gx(qht)
-        qm = cholqr_mixed(ops, t, y, m, k, kp, final=it == q - 1)
+        qm = cholqr_mixed(ops, t, y, m, k, kp, final=it == q - 1, reduce=reduce,
+                          rows_total=mt)
     b = pass_gtq(qm).contiguous()
     energy = ops.sumsq(_dev.vp(b), ldn, k, n)
     if int(ops.status.item()) & ST_CHOL:

@@ -155,3 +155,60 @@ def test_tf32_pair_compare_within_cfg4_tolerance(rg):
     _, theta, _, _, d1, d2 = orc.comparative(o.alphas, o.betas, o.r)
     assert np.max(np.abs(r32.theta - theta)) <= 1e-4
     assert abs(r32.d1 - d1) <= 1e-4 and abs(r32.d2 - d2) <= 1e-4
+
+
+def test_f32_row_sharded_chain_two_shards(rg):
+    """The row-sharded tf32 chain (dist.sharded_chain_f32's math): two row
+    shards of one fp32 matrix, each run by its own host thread, with every
+    partial (||G||^2, Grams, Z^T, B) summed across the shards by a host-side
+    stand-in for the NCCL all-reduce. The replicated B must match the
+    unsharded chain's at fp32-level accuracy."""
+    import threading
+
+    g1, _ = _f32_pair(m=4000, n=300)
+    k, q, seed = 24, 1, 7
+    m = g1.shape[0]
+    full = rg.device.to_device(torch.from_numpy(g1).cuda(), "g", keep_f32=True)
+    _, b_ref, h_ref = rg.tf32.tf32_chain(full, k, q, seed)
+    cut = 1700
+    shards = [torch.from_numpy(np.ascontiguousarray(g1[:cut])).cuda(),
+              torch.from_numpy(np.ascontiguousarray(g1[cut:])).cuda()]
+    bar = threading.Barrier(2)
+    slots = [None, None]
+    out = [None, None]
+    errs = []
+
+    def make_reduce(r):
+        def reduce(t):
+            torch.cuda.synchronize()
+            slots[r] = t.clone()
+            bar.wait()
+            t.copy_(slots[0] + slots[1])
+            torch.cuda.synchronize()
+            bar.wait()
+            return t
+        return reduce
+
+    def run(r):
+        try:
+            a = rg.device.to_device(shards[r], "g", keep_f32=True)
+            out[r] = rg.tf32.tf32_chain(a, k, q, seed, reduce=make_reduce(r), rows_total=m)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    b0, b1 = out[0][1].cpu().numpy(), out[1][1].cpu().numpy()
+    assert np.array_equal(b0, b1)  # replicated after the all-reduce
+    br = b_ref.cpu().numpy()
+    ss = CONFIGS["cfg4"].s // 2 if CONFIGS["cfg4"].s // 2 < k else k // 2
+    assert np.linalg.norm(b0[:ss] - br[:ss]) <= 1e-5 * np.linalg.norm(br[:ss])
+    e_s = out[0][2][0] ** 2 - out[0][2][1] ** 2
+    e_r = h_ref[0] ** 2 - h_ref[1] ** 2
+    assert abs(e_s - e_r) <= 2e-6 * e_r
+    assert abs(out[0][2][0] - h_ref[0]) <= 1e-13 * h_ref[0]
