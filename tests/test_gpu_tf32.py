@@ -212,3 +212,29 @@ def test_f32_row_sharded_chain_two_shards(rg):
     e_r = h_ref[0] ** 2 - h_ref[1] ** 2
     assert abs(e_s - e_r) <= 2e-6 * e_r
     assert abs(out[0][2][0] - h_ref[0]) <= 1e-13 * h_ref[0]
+
+
+@pytest.mark.parametrize("m,p,n,k,q", [(300, 200, 64, 16, 1), (1000, 900, 301, 20, 1),
+                                       (129, 150, 100, 40, 0), (2000, 1500, 256, 100, 2)])
+def test_tf32_pair_edge_shapes(rg, m, p, n, k, q):
+    """kp not a multiple of 32 (zero-padded tensor-core operands), odd n
+    (ld % 4 != 0: the promoted fp64 chain serves it), a single 128-row tile,
+    two output chunks (kp = 112 -> 128, one CTA) and q = 0 / 2."""
+    cfg = CONFIGS["cfg4"]
+    g1, g2 = make_pair(cfg, data_seed=m + n, m=m, p=p, n=n)
+    g1, g2 = g1.astype(np.float32), g2.astype(np.float32)
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(k, 2, q))
+    rep = rg.compare(rg.GmpPair(g1, g2, check_rank=False), opts)
+    o = orc.run_pipeline(g1.astype(np.float64), g2.astype(np.float64), k=k, q=q, seed=2)
+    assert (rep.spectrum.r, rep.spectrum.s) == (o.r, o.s)
+    assert np.max(np.abs(rep.spectrum.alphas - o.alphas)) <= 1e-4
+    _, theta, _, _, d1, d2 = orc.comparative(o.alphas, o.betas, o.r)
+    assert np.max(np.abs(rep.theta - theta)) <= 1e-4
+    assert abs(rep.d1 - d1) <= 1e-4 and abs(rep.d2 - d2) <= 1e-4
+    dm = rg.device.to_device(torch.from_numpy(g1).cuda(), "g", keep_f32=True)
+    assert rg.tf32.supported(dm, k) == (n % 4 == 0)
+    if n % 4 == 0:
+        _, _, h = rg.tf32.tf32_chain(dm, k, q, 2)
+        ob = orc.fixed_rank_basis(g1.astype(np.float64), k, q, 2)
+        e, eo = h[0] ** 2 - h[1] ** 2, orc.sum_sq(ob.b)
+        assert abs(e - eo) <= 5e-6 * eo
