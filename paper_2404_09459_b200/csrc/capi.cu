@@ -93,6 +93,15 @@ int make_tmap_2d_swz(CUtensorMap* out, const void* base, uint64_t inner, uint64_
 }
 
 static inline int64_t ceil16(int64_t x) { return (x + 15) / 16 * 16; }
+// Split cap of the Z^T / B = Q^T G reductions (RGSV_PROJ_SPLIT; tuning).
+static int proj_split() {
+  static const int v = [] {
+    const char* e = getenv("RGSV_PROJ_SPLIT");
+    const int x = e ? atoi(e) : 0;
+    return x >= 1 ? x : kSMs;
+  }();
+  return v;
+}
 constexpr int kIntermediatePasses = 3;  // see the note in rgsv_sketch_project
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -366,7 +375,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
     p.K = m;
     p.scratch = scratch;
     p.scratch_bytes = sb;
-    p.max_split = kSMs;
+    p.max_split = proj_split();
     if (int e = gemm_gtq(p, st)) return e;
     double* qt = nullptr;
     if (int e = cholqr3_wide(z, z2, n, ldn, k, (int)kp, gram, linv, rinv, rd_ws, scratch, sb,
@@ -395,7 +404,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
   p.K = m;
   p.scratch = scratch;
   p.scratch_bytes = sb;
-  p.max_split = kSMs;
+  p.max_split = proj_split();
   if (int e = gemm_gtq(p, st)) return e;
   if (int e = launch_sumsq(b_out, ldb, kp, n, stats + 1, ss, 1024, st)) return e;
   if (rdiag) {

@@ -1106,6 +1106,20 @@ int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
+// Split count of the tall Gram Y^T Y (K = m rows, kp x kp output): the
+// reduction over rows is the only parallelism. 32 splits: measured on cfg1
+// (8 concurrent pairs) 684 / 698 / 713 / 718 pairs/s at 148 / 74 / 32 / 16
+// splits and 2.24 / 2.25 / 2.31 / 2.52 ms single-pair latency.
+// RGSV_GRAM_SPLIT overrides it (tuning experiments).
+static int tall_gram_split() {
+  static const int v = [] {
+    const char* e = getenv("RGSV_GRAM_SPLIT");
+    const int x = e ? atoi(e) : 0;
+    return x >= 1 ? x : 32;
+  }();
+  return v;
+}
+
 int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram, double* linv,
                  double* rdiag, double* scratch, size_t scratch_bytes, int* status,
                  double** q_out, cudaStream_t st, int passes) {
@@ -1124,7 +1138,7 @@ int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram,
     g.K = m;
     g.scratch = scratch;
     g.scratch_bytes = scratch_bytes;
-    g.max_split = kSMs;
+    g.max_split = tall_gram_split();
     if (int e = gemm_gtq(g, st)) return e;
     if (int e = chol_inv(gram, k, kp, step == 0 ? m : 0, linv, nullptr, nullptr,
                          step == 0 ? rdiag : nullptr, step == 0 ? nullptr : rdiag, status, st))

@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "rgsv_internal.h"
@@ -100,6 +101,14 @@ RGSV_DI void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// L2 prefetch of a 2-D tensor tile (no shared-memory destination).
+RGSV_DI void tma_prefetch_l2(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y)
+               : "memory");
+}
+
 RGSV_DI float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_tf32x3(const __grid_constant__ CUtensorMap tg, const __grid_constant__ CUtensorMap tglo,
              const __grid_constant__ CUtensorMap tbh, const __grid_constant__ CUtensorMap tbl,
              double* __restrict__ out, int64_t ldo, int64_t split_stride, int M, int N, int K,
-             int rows_per, int c0w, int stages, int flush) {
+             int rows_per, int c0w, int stages, int flush, int pf) {
   constexpr bool GX = MODE == kGX;
   constexpr uint32_t SW = GX ? BK * 4 : 128;   // bytes per swizzled smem row
   constexpr uint32_t BOX = BK * 128;           // kGTQ: one 32-column box
@@ -212,6 +221,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* st = R.base + (size_t)s * stage_bytes;
         mbar_arrive_expect_tx(R.full + s, stage_bytes);
         const int kk = r0 + kb * BK;
+        // the G tiles come from HBM: prefetch them into L2 `pf` K-blocks ahead
+        // (chunk 0 of a tile only; chunk 1 re-reads them from L2)
+        const int kpf = kb + pf;
+        if (pf > 0 && chunk == 0 && kpf < nkb) {
+          const int kq = r0 + kpf * BK;
+          if (GX) {
+            tma_prefetch_l2(&tg, kq, m0);
+            tma_prefetch_l2(&tglo, kq, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              tma_prefetch_l2(&tg, m0 + 32 * j, kq);
+              tma_prefetch_l2(&tglo, m0 + 32 * j, kq);
+            }
+          }
+        }
         if (GX) {
           tma_load_2d(st, &tg, R.full + s, kk, m0);
           tma_load_2d(st + a_bytes, &tglo, R.full + s, kk, m0);
@@ -422,6 +447,10 @@ int g_bk_gx = 32;   // K-block (16: 64B swizzle rows, 32: 128B) of the gx kernel
 int g_bk_gtq = 32;  // K-block (rows) of the gtq kernel
 int g_rows_per_split = 8192;
 int g_flush = 2;    // K-blocks accumulated in TMEM before an fp32 register flush
+// L2 prefetch distance of the G tiles in K-blocks (0: off). Measured at cfg4
+// (tools/tf32_sweep.py): gx 174 / 167 / 160 / 162 TFLOP/s at 0 / 2 / 4 / 8, so
+// HBM latency is not the limiter; off by default (RGSV_TF32_PREFETCH).
+int g_prefetch = 0;
 
 template <int MODE, int BK>
 int launch_bk(const CUtensorMap& tg, const CUtensorMap& tgl, const CUtensorMap& tbh,
@@ -436,7 +465,7 @@ int launch_bk(const CUtensorMap& tg, const CUtensorMap& tgl, const CUtensorMap& 
       cudaSuccess)
     return RGSV_ERR_CUDA;
   kern<<<grid, kThreads, smem, st>>>(tg, tgl, tbh, tbl, out, ldo, split_stride, M, N, K, rows_per,
-                                     first_chunk(N), stages, g_flush);
+                                     first_chunk(N), stages, g_flush, g_prefetch);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
@@ -509,6 +538,7 @@ extern "C" {
 
 int rgsv_tf32_config(int bk_gx, int bk_gtq, int rows_per_split, int flush) {
   if (flush >= 1) g_flush = flush;
+  if (const char* e = getenv("RGSV_TF32_PREFETCH")) g_prefetch = atoi(e);
   if (bk_gx == 16 || bk_gx == 32) g_bk_gx = bk_gx;
   if (bk_gtq == 8 || bk_gtq == 16 || bk_gtq == 32) g_bk_gtq = bk_gtq;
   if (rows_per_split >= 64) g_rows_per_split = rows_per_split;

@@ -36,11 +36,15 @@ def tm(fn, reps=3):
     return e0.elapsed_time(e1) / reps * 1e-3
 
 
-for bk, bq, rps, fl in [(16, 16, 8192, 1), (32, 16, 8192, 1), (16, 32, 8192, 1), (16, 8, 8192, 1),
-                        (16, 16, 8192, 2), (16, 16, 8192, 4), (16, 16, 16384, 1),
-                        (16, 16, 4096, 1), (32, 32, 8192, 2)]:
+configs = [(32, 32, 8192, 2, pf) for pf in (0, 2, 4, 8, 16)]
+if os.environ.get("FULL_SWEEP"):
+    configs = [(16, 16, 8192, 1, 0), (32, 16, 8192, 1, 0), (16, 32, 8192, 1, 0),
+               (16, 16, 8192, 2, 0), (32, 32, 8192, 1, 0), (32, 32, 8192, 2, 0)] + configs
+for bk, bq, rps, fl, pf in configs:
+    os.environ["RGSV_TF32_PREFETCH"] = str(pf)
     L.rgsv_tf32_config(bk, bq, rps, fl)
     tgx = tm(lambda: o.gx(a, lo, xh, xl, y, m, kq, n))
     tgq = tm(lambda: o.gtq(qh, ql, a, lo, z, kq, n, m))
-    print(f"bk_gx={bk} bk_gtq={bq} rows/split={rps} flush={fl}: gx {tgx*1e3:.2f} ms "
-          f"({flop/tgx/1e12:.1f} TF/s)  gtq {tgq*1e3:.2f} ms ({flop/tgq/1e12:.1f} TF/s)", flush=True)
+    print(f"bk_gx={bk} bk_gtq={bq} rows/split={rps} flush={fl} l2_prefetch={pf}: gx "
+          f"{tgx*1e3:.2f} ms ({flop/tgx/1e12:.1f} TF/s)  gtq {tgq*1e3:.2f} ms "
+          f"({flop/tgq/1e12:.1f} TF/s)", flush=True)
