@@ -33,6 +33,11 @@ def test_config_validation_mirrors_reference():
         GsvOptions(classify_tol=0.5)
     with pytest.raises(ValidationError):
         GsvOptions(method="magic")
+    # fp32 compute mode (not in the reference, which promotes to fp64)
+    assert GsvOptions().f32_mode == "tf32x3"
+    assert GsvOptions(f32_mode="promote").f32_mode == "promote"
+    with pytest.raises(ValidationError):
+        GsvOptions(f32_mode="fp16")
 
 
 def test_single_block_detection():
@@ -201,3 +206,25 @@ def test_bench_reference_arm_contract():
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def test_sharded_bench_mode_is_wired():
+    """bench.py --sharded routes cfg2/cfg4 to the row-sharded strong-scaling
+    driver (dist.compute_gsv_sharded); the fp32 shards take the tf32 chain."""
+    import os
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    from paper_2404_09459_b200 import dist as rdist
+
+    sys.argv = ["bench.py", "--sharded", "--config", "cfg4"]
+    args = bench.parse()
+    assert args.sharded and args.config == "cfg4"
+    assert callable(bench.run_ours_sharded) and callable(rdist.sharded_chain_f32)
+    # balanced contiguous gene blocks of the genome-scale configs
+    for cfg in ("cfg2", "cfg4"):
+        m = CONFIGS[cfg].m
+        blocks = [rdist.shard_rows(m, r, 8) for r in range(8)]
+        assert blocks[0][0] == 0 and blocks[-1][1] == m

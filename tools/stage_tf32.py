@@ -52,12 +52,13 @@ for rep in range(2):
         return out[:kp]
 
     y = pass_gx(om)
-    qm = t("cholqr3 tall", lambda: ops.cholqr3(y, m, k, kp))
-    for _ in range(q):
+    qm = t("cholqr mixed (2 pass)", lambda: tf.cholqr_mixed(ops, o, y, m, k, kp, final=q == 0))
+    for it in range(q):
         zt = pass_gtq(qm)
         qht = t("cholqr3 wide", lambda: ops.wide_cholqr3(zt.contiguous(), n, ldn, k, kp))
         y = pass_gx(qht)
-        qm = t("cholqr3 tall", lambda: ops.cholqr3(y, m, k, kp))
+        qm = t("cholqr mixed (final)",
+               lambda: tf.cholqr_mixed(ops, o, y, m, k, kp, final=it == q - 1))
     b = pass_gtq(qm).contiguous()
     t("sumsq B", lambda: ops.sumsq(dv.vp(b), ldn, k, n))
     t("small GSVD + comparative", lambda: dv.small_spectrum(b, k, b, k, n, 1e-10))
