@@ -48,10 +48,11 @@ class GmpPair:
     finiteness (device pass) and m + p >= n. Like the reference it checks
     sigma_min > 1e-12 sigma_max of the stacked pair (engine.py:55-61), on the
     device (validation.py). ``check_rank=None`` (default) runs that check
-    whenever the device kernels cover it (n <= 512: every reference test
-    shape) and skips it for the genome-scale configs, which the reference's
-    own benchmark plan also builds unvalidated (SURVEY.md §8(d));
-    True forces it (DimensionError beyond its limits), False skips it."""
+    whenever it is cheap (n <= 512: every reference test shape) and skips
+    it for the larger configs, which the reference's own benchmark plan also
+    builds unvalidated; True forces it (up to n = 1024
+    through the blocked Cholesky, ~3 s at cfg1's 36000 x 1000; DimensionError
+    beyond), False skips it."""
 
     g1: object
     g2: object

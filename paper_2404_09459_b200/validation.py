@@ -4,7 +4,7 @@ The reference takes the singular values of vstack(G1, G2) with a dense
 LAPACK SVD. Here the singular values come from one-sided Jacobi on the
 device: directly on the stacked matrix when it is small, otherwise on the
 R factor of a shifted CholeskyQR3 of the stacked pair (same singular
-values; n <= 512, the single-CTA Cholesky limit).
+values; n <= 1024, the blocked Cholesky limit).
 """
 
 from __future__ import annotations
@@ -44,8 +44,8 @@ def stacked_extreme_singular_values(g1: "_dev.DevMatrix", g2: "_dev.DevMatrix"):
     from .core import _qr_in_place
 
     kp = _dev.ceil16(n)
-    if kp > 512:
-        raise DimensionError("check_rank supports n <= 512 for large stacked pairs")
+    if kp > 1024:
+        raise DimensionError("check_rank supports n <= 1024 for large stacked pairs")
     y = torch.zeros((rows, kp), dtype=torch.float64, device="cuda")
     y[: g1.rows, :n].copy_(g1.t)
     y[g1.rows:, :n].copy_(g2.t)

@@ -233,3 +233,23 @@ def test_batch_equals_single():
     e_ref = orc.sum_sq(ob.b)
     h = run[1].basis1.residual_history
     assert abs(h[0] ** 2 - h[1] ** 2 - e_ref) <= 1e-12 * e_ref
+
+
+def test_rank_check_wide_blocked_cholesky():
+    """check_rank=True beyond the one-CTA Cholesky (512 < n <= 1024): the R
+    factor comes through the blocked Cholesky; sigma_max / sigma_min agree
+    with LAPACK and a rank-deficient stacked pair is rejected like
+    engine.py:55-61."""
+    rng = np.random.default_rng(3)
+    n = 600
+    g1 = rng.standard_normal((2000, n))
+    g2 = rng.standard_normal((900, n))
+    pair = rg.GmpPair(g1, g2, check_rank=True)
+    s = np.linalg.svd(np.vstack([g1, g2]), compute_uv=False)
+    assert abs(pair.stack_norm2 - s[0]) <= 1e-12 * s[0]
+    assert abs(pair.stack_pinv_norm - 1 / s[-1]) <= 1e-10 / s[-1]
+    # a stacked pair of rank n - 1 (column n-1 = column 0 + column 1)
+    g1[:, -1] = g1[:, 0] + g1[:, 1]
+    g2[:, -1] = g2[:, 0] + g2[:, 1]
+    with pytest.raises(rg.RankDeficiencyError):
+        rg.GmpPair(g1, g2, check_rank=True)
