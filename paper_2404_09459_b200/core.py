@@ -76,7 +76,7 @@ def frobenius_norm(m) -> float:
 
 
 def reduced_qr(m) -> QrFactors:
-    """Reduced QR of a tall full-column-rank matrix (cols <= 512) by shifted
+    """Reduced QR of a tall full-column-rank matrix (cols <= 1024) by shifted
     CholeskyQR3 on the B200; R has a positive diagonal, which is the
     reference's phase convention (core.py:79-96)."""
     g = as_matrix(m)
@@ -84,8 +84,8 @@ def reduced_qr(m) -> QrFactors:
     if rows < cols:
         raise DimensionError("B200 reduced_qr supports tall matrices (rows >= cols)")
     kp = _dev.ceil16(cols)
-    if kp > 512:
-        raise DimensionError("B200 reduced_qr supports at most 512 columns")
+    if kp > 1024:
+        raise DimensionError("B200 reduced_qr supports at most 1024 columns")
     y = torch.zeros((rows, kp), dtype=torch.float64, device="cuda")
     y[:, :cols].copy_(g.t[:, :cols])
     r = _qr_in_place(y, rows, cols)

@@ -527,7 +527,7 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
   } else {
     // tall stacked matrix (l > n): Q = qr(S).q directly
     const int64_t kpn = L.kpn;
-    if (kpn > 512) return RGSV_ERR_DIMENSION;
+    if (kpn > 1024) return RGSV_ERR_DIMENSION;  // blocked Cholesky limit
     if (int e = launch_stack(S, kpn, b1, ldb1, l1, b2, ldb2, l2, l, n, st)) return e;
     if (int e = cholqr3_tall(S, S2, l, (int)n, (int)kpn, gram, linv, rdiag, scratch, sb, status,
                              &Q, st))

@@ -15,8 +15,8 @@ C1 = Q1ᵀG1, C2 = Q2ᵀG2 (or G1, G2 themselves for method="direct"):
 
 All arithmetic runs in librgsv_b200.so; torch only allocates, slices and
 flips buffers. Meaningful in the adaptive / direct regime, where
-l1 + l2 >= n; the stacked width n is limited to 512
-(the one-CTA Cholesky / Jacobi kernels).
+l1 + l2 >= n; the stacked width n is limited to 1024
+(the blocked Cholesky and the one-CTA Householder / Jacobi kernels).
 """
 
 from __future__ import annotations
@@ -172,8 +172,8 @@ def recover(pair, opts, direct: bool):
     if min(l, n) != n:                                   # engine.py:309-313
         raise RecoveryError("compressed pair has fewer than n independent columns; "
                             "tighten the extraction tolerance")
-    if n > 512:
-        raise RecoveryError(f"device recovery supports n <= 512, got n={n}")
+    if n > 1024:
+        raise RecoveryError(f"device recovery supports n <= 1024, got n={n}")
     spec: GsvSpectrum = _spectrum_checked(c1, l1, c2, l2, n, opts.classify_tol)
     alphas, betas, r, s = spec.alphas, spec.betas, spec.r, spec.s
     tol = opts.classify_tol

@@ -117,3 +117,17 @@ def test_recovered_spectrum_matches_oracle(rg):
     al, be, r, s, *_ = orc.spectrum_from_l_blocks(qf[:50], qf[50:], 40, 1e-10)
     assert np.max(np.abs(fac.spectrum.alphas - al)) <= 1e-12
     assert (fac.spectrum.r, fac.spectrum.s) == (r, s)
+
+
+@pytest.mark.parametrize("method", ["direct", "randomized"])
+def test_wide_pair_blocked_cholesky(rg, method):
+    """n = 600 > 512: the stacked QR and every CholeskyQR go through the
+    blocked Cholesky (kp > 128); the reference's recovery invariants hold."""
+    m, p, n = 900, 700, 600
+    g1, g2 = orc.gaussian_matrix(m, n, 21), orc.gaussian_matrix(p, n, 22)
+    pair = rg.GmpPair(g1, g2, check_rank=False)
+    fac = rg.recover_gsvd(pair, rg.GsvOptions(
+        method=method, extraction=rg.ExtractionConfig(tol=1e-12, seed=21)))
+    _check_factors(pair, fac, g1, g2)
+    qf = rg.reduced_qr(g1)
+    assert np.linalg.norm(qf.q @ qf.r - g1) <= 1e-12 * np.linalg.norm(g1)
