@@ -371,16 +371,31 @@ __global__ void __launch_bounds__(256) k_split_f32(const float* __restrict__ g, 
     const float* src = g + r * ldg;
     float* dst = lo + r * ldl;
     if (vec) {
-      for (int c = lane * 4; c < cols; c += 128) {
-        float4 x = __ldcs(reinterpret_cast<const float4*>(src + c));
-        float e[4] = {x.x, x.y, x.z, x.w};
+      // 4 independent 16-byte loads in flight per lane (HBM-bound pass)
+      for (int c0 = lane * 4; c0 < cols; c0 += 512) {
+        float4 x[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float h = mode ? tf32_rna(e[t]) : __uint_as_float(__float_as_uint(e[t]) & 0xFFFFE000u);
-          acc = fma((double)e[t], (double)e[t], acc);
-          e[t] = tf32_rna(e[t] - h);
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * 128;
+          x[u] = c < cols ? __ldcs(reinterpret_cast<const float4*>(src + c))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        __stcs(reinterpret_cast<float4*>(dst + c), make_float4(e[0], e[1], e[2], e[3]));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * 128;
+          float e[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+          double sq = 0.0;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float h =
+                mode ? tf32_rna(e[t]) : __uint_as_float(__float_as_uint(e[t]) & 0xFFFFE000u);
+            sq = fma((double)e[t], (double)e[t], sq);
+            e[t] = tf32_rna(e[t] - h);
+          }
+          acc += sq;
+          if (c < cols)
+            __stcs(reinterpret_cast<float4*>(dst + c), make_float4(e[0], e[1], e[2], e[3]));
+        }
       }
     } else {
       for (int c = lane; c < cols; c += 32) {
@@ -417,19 +432,24 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int n, double
 }
 
 // hi = tf32(x), lo = tf32(x - hi) of an fp64 matrix, zero in columns
-// [cols, cols_out) (padding read by the MMAs).
-__global__ void k_split_f64(const double* __restrict__ x, int64_t ldx, int64_t rows, int cols,
-                            float* __restrict__ hi, float* __restrict__ lo, int64_t ldo,
-                            int cols_out) {
-  const int64_t total = rows * cols_out;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx / cols_out;
-    const int c = (int)(idx % cols_out);
-    const double v = c < cols ? x[r * ldx + c] : 0.0;
-    const float h = tf32_rna((float)v);
-    hi[r * ldo + c] = h;
-    lo[r * ldo + c] = tf32_rna((float)(v - (double)h));
+// [cols, cols_out) (padding read by the MMAs). One warp per row (grid-stride
+// over rows), lanes over columns: no per-element division, coalesced.
+__global__ void __launch_bounds__(256) k_split_f64(const double* __restrict__ x, int64_t ldx,
+                                                   int64_t rows, int cols,
+                                                   float* __restrict__ hi,
+                                                   float* __restrict__ lo, int64_t ldo,
+                                                   int cols_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < rows; r += (int64_t)gridDim.x * 8) {
+    const double* src = x + r * ldx;
+    float* ph = hi + r * ldo;
+    float* pl = lo + r * ldo;
+    for (int c = lane; c < cols_out; c += 32) {
+      const double v = c < cols ? __ldcs(src + c) : 0.0;
+      const float h = tf32_rna((float)v);
+      ph[c] = h;
+      pl[c] = tf32_rna((float)(v - (double)h));
+    }
   }
 }
 
@@ -568,7 +588,9 @@ int rgsv_f64_split_tf32(const double* x, int64_t ldx, int64_t rows, int64_t cols
     return RGSV_ERR_DIMENSION;
   if (rows == 0 || cols_out == 0) return 0;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  k_split_f64<<<kSMs * 8, 256, 0, st>>>(x, ldx, rows, (int)cols, hi, lo, ldo, (int)cols_out);
+  int blocks = (int)((rows + 7) / 8);
+  if (blocks > kSMs * 16) blocks = kSMs * 16;
+  k_split_f64<<<blocks, 256, 0, st>>>(x, ldx, rows, (int)cols, hi, lo, ldo, (int)cols_out);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
