@@ -342,6 +342,208 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// gx on CTA PAIRS (tcgen05 cta_group::2): a 2-CTA cluster computes a 256-row
+// tile; each CTA stages its own 128 rows of G (+ lo) and HALF of the X chunk,
+// and the leader's single thread issues M = 256 MMAs that read both CTAs'
+// shared memory and write both CTAs' TMEM. Per SM this halves the staged X
+// bytes (52 instead of 72 KB per 32-deep K-block, 4 stages instead of 3).
+// Barriers: full[] live in the leader (both CTAs' TMA bytes land there;
+// count 2 = leader expect_tx + peer arrive); empty[] and sfull[] in both CTAs
+// (leader's multicast commits); sempty[] in the leader (16 epilogue warps).
+RGSV_DI uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+RGSV_DI void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+RGSV_DI uint32_t mapa_u32(const void* local, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  return ra;
+}
+RGSV_DI void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// 2-SM TMA: the transaction bytes complete on the LEADER's barrier (peer bit
+// of the barrier address cleared), the data lands in this CTA's smem.
+RGSV_DI void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+RGSV_DI void mma_tf32_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+RGSV_DI void mma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int BK>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tf32x3_gx2(const __grid_constant__ CUtensorMap tg, const __grid_constant__ CUtensorMap tglo,
+                 const __grid_constant__ CUtensorMap tbh, const __grid_constant__ CUtensorMap tbl,
+                 double* __restrict__ out, int64_t ldo, int M, int N, int K, int c0w, int stages,
+                 int flush) {
+  constexpr uint32_t SW = BK * 4;
+  constexpr uint32_t LAYOUT = BK == 16 ? 4u : 2u;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t rank = cta_rank();
+  const int nchunk = N > c0w ? 2 : 1;
+  const int pair = blockIdx.x >> 1;
+  const int chunk = pair % nchunk;
+  const int col0 = chunk ? c0w : 0;
+  const int W = chunk ? N - c0w : c0w;   // MMA N (both CTAs' halves)
+  const int hb = c0w / 2;                // staged X rows per CTA (box)
+  const uint32_t a_bytes = kTileM * SW;
+  const uint32_t b_bytes = (uint32_t)hb * SW;
+  const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  Smem R = carve(smem_raw, stages, stage_bytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = (pair / nchunk) * 2 * kTileM + (int)rank * kTileM;
+  const int xrow0 = col0 + (int)rank * (W / 2);
+  const int nkb = (K + BK - 1) / BK;
+  const int ns = min(kMaxSlots, (int)(kTmemCols / c0w));
+  const int ngroups = (nkb + flush - 1) / flush;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(R.full + s, 2);
+      mbar_init(R.empty + s, 1);
+    }
+    for (int s = 0; s < kMaxSlots; ++s) {
+      mbar_init(R.sfull + s, 1);
+      mbar_init(R.sempty + s, 2 * kEpiWarps);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tg);
+    tma_prefetch(&tglo);
+    tma_prefetch(&tbh);
+    tma_prefetch(&tbl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(R.tslot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tbase = *R.tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_leader = mapa_u32(R.full, 0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % stages;
+        const uint32_t ph = (uint32_t)(kb / stages) & 1u;
+        mbar_wait(R.empty + s, ph ^ 1u);
+        uint8_t* st = R.base + (size_t)s * stage_bytes;
+        if (rank == 0)
+          mbar_arrive_expect_tx(R.full + s, 2 * stage_bytes);
+        else
+          mbar_arrive_remote(full_leader + (uint32_t)s * 8u);
+        const int kk = kb * BK;
+        tma_load_2d_2sm(st, &tg, R.full + s, kk, m0);
+        tma_load_2d_2sm(st + a_bytes, &tglo, R.full + s, kk, m0);
+        tma_load_2d_2sm(st + 2 * a_bytes, &tbh, R.full + s, kk, xrow0);
+        tma_load_2d_2sm(st + 2 * a_bytes + b_bytes, &tbl, R.full + s, kk, xrow0);
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      const uint32_t id = idesc_tf32(2 * kTileM, W, 0, 0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % stages;
+        const uint32_t ph = (uint32_t)(kb / stages) & 1u;
+        const int t = kb / flush;
+        const int slot = t % ns;
+        const bool first = (kb % flush) == 0;
+        const bool last = (kb % flush) == flush - 1 || kb == nkb - 1;
+        if (first) mbar_wait(R.sempty + slot, ((uint32_t)(t / ns) & 1u) ^ 1u);
+        mbar_wait(R.full + s, ph);
+        tc_fence_after();
+        const uint32_t a = smem_u32(R.base + (size_t)s * stage_bytes);
+        const uint32_t alo = a + a_bytes, bh = a + 2 * a_bytes, bl = bh + b_bytes;
+        const uint32_t td = tbase + (uint32_t)(slot * c0w);
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const uint32_t ko = (uint32_t)k * 32u;
+          const uint64_t dA = umma_desc(a + ko, 16, 8 * SW, LAYOUT);
+          const uint64_t dAl = umma_desc(alo + ko, 16, 8 * SW, LAYOUT);
+          const uint64_t dBh = umma_desc(bh + ko, 16, 8 * SW, LAYOUT);
+          const uint64_t dBl = umma_desc(bl + ko, 16, 8 * SW, LAYOUT);
+          mma_tf32_2sm(td, dA, dBh, id, (!first || k > 0) ? 1u : 0u);
+          mma_tf32_2sm(td, dA, dBl, id, 1u);
+          mma_tf32_2sm(td, dAl, dBh, id, 1u);
+        }
+        if (last) mma_commit_2sm(R.sfull + slot);
+        mma_commit_2sm(R.empty + s);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int hw = W / 2;
+    float acc[kMaxHalf];
+#pragma unroll
+    for (int j = 0; j < kMaxHalf; ++j) acc[j] = 0.f;
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * hw);
+    const uint32_t sempty_leader = mapa_u32(R.sempty, 0);
+    for (int t = 0; t < ngroups; ++t) {
+      const int slot = t % ns;
+      mbar_wait(R.sfull + slot, (uint32_t)(t / ns) & 1u);
+      tc_fence_after();
+      const uint32_t src = lane_base + (uint32_t)(slot * c0w);
+#pragma unroll
+      for (int j0 = 0; j0 < kMaxHalf; j0 += 16) {
+        if (j0 < hw) {
+          float v[16];
+          tmem_ld16(src + (uint32_t)j0, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[j0 + i] += v[i];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(sempty_leader + (uint32_t)slot * 8u);
+    }
+    const int idx = m0 + q * 32 + lane;
+    if (idx < M) {
+      double* dst = out + (int64_t)idx * ldo + col0 + h * hw;
+#pragma unroll
+      for (int j = 0; j < kMaxHalf; j += 2)
+        if (j < hw) *reinterpret_cast<double2*>(dst + j) = make_double2(acc[j], acc[j + 1]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
 // out[j][i] = sum_s ws[s][j][i] in split order (deterministic).
 __global__ void k_sum_splits(const double* __restrict__ ws, int S, int64_t stride, int N, int M,
                              int64_t ldw, double* __restrict__ out, int64_t ldo) {
@@ -506,6 +708,50 @@ int launch_gx_bk(const float* g, const float* glo, int64_t ldg, const float* xh,
   return launch_bk<kGX, BK>(tg, tgl, txh, txl, stage, dim3(tiles), y, ldy, 0, M, N, K, K, st);
 }
 
+// 2-SM launch of gx (RGSV_TF32_2SM=1; needs N chunks whose halves are
+// multiples of 8 rows).
+template <int BK>
+int launch_gx2_bk(const float* g, const float* glo, int64_t ldg, const float* xh,
+                  const float* xl, int64_t ldx, double* y, int64_t ldy, int M, int N, int K,
+                  cudaStream_t st) {
+  constexpr int SW = BK * 4;
+  const int c0w = first_chunk(N);
+  if ((c0w / 2) % 8 || ((N - c0w) > 0 && ((N - c0w) / 2) % 8)) return RGSV_ERR_DIMENSION;
+  CUtensorMap tg, tgl, txh, txl;
+  if (make_tmap_2d_swz(&tg, g, K, M, ldg, BK, kTileM, 4, SW) ||
+      make_tmap_2d_swz(&tgl, glo, K, M, ldg, BK, kTileM, 4, SW) ||
+      make_tmap_2d_swz(&txh, xh, K, N, ldx, BK, c0w / 2, 4, SW) ||
+      make_tmap_2d_swz(&txl, xl, K, N, ldx, BK, c0w / 2, 4, SW))
+    return RGSV_ERR_CUDA;
+  const uint32_t stage = 2u * kTileM * SW + 2u * (uint32_t)(c0w / 2) * SW;
+  int stages = (int)((kSmemMax - kSmemReserve) / stage);
+  if (stages > 8) stages = 8;
+  if (stages < 2) return RGSV_ERR_DIMENSION;
+  const uint32_t smem = (uint32_t)stages * stage + kSmemReserve;
+  auto kern = k_tf32x3_gx2<BK>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return RGSV_ERR_CUDA;
+  const int pairs = (M + 2 * kTileM - 1) / (2 * kTileM) * (N > c0w ? 2 : 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, tg, tgl, txh, txl, y, ldy, M, N, K, c0w, stages, g_flush) !=
+      cudaSuccess)
+    return RGSV_ERR_CUDA;
+  note_launch();
+  return 0;
+}
+
 template <int BK>
 int launch_gtq_bk(const float* q, const float* ql, int64_t ldq, const float* g, const float* glo,
                   int64_t ldg, double* c, int64_t ldc, int N, int M, int K, void* scratch,
@@ -605,6 +851,11 @@ int rgsv_tf32x3_gx(const float* g, const float* glo, int64_t ldg, const float* x
     return RGSV_ERR_DIMENSION;
   if (M == 0) return 0;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // opt-in 2-SM variant (measured 161 vs 169 TFLOP/s for the 1-SM kernel at
+  // cfg4, tools/tf32_sweep.py), read per call so tests can exercise both
+  const char* e2 = getenv("RGSV_TF32_2SM");
+  if (e2 && atoi(e2) == 1 && g_bk_gx == 32)
+    return launch_gx2_bk<32>(g, glo, ldg, xhi, xlo, ldx, y, ldy, (int)M, (int)N, (int)K, st);
   if (g_bk_gx == 32)
     return launch_gx_bk<32>(g, glo, ldg, xhi, xlo, ldx, y, ldy, (int)M, (int)N, (int)K, st);
   return launch_gx_bk<16>(g, glo, ldg, xhi, xlo, ldx, y, ldy, (int)M, (int)N, (int)K, st);

@@ -238,3 +238,20 @@ def test_tf32_pair_edge_shapes(rg, m, p, n, k, q):
         ob = orc.fixed_rank_basis(g1.astype(np.float64), k, q, 2)
         e, eo = h[0] ** 2 - h[1] ** 2, orc.sum_sq(ob.b)
         assert abs(e - eo) <= 5e-6 * eo
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 64, 300), (777, 288, 1000), (300, 320, 200)])
+def test_gx_cta_pair_variant(rg, M, N, K, monkeypatch):
+    """The opt-in 2-SM gx (tcgen05 cta_group::2: a CTA pair computes a
+    256-row tile, each CTA staging half of X; RGSV_TF32_2SM=1) gives the
+    same fp32-level accuracy as the 1-SM kernel."""
+    rng = np.random.default_rng(M * 7 + N)
+    g32 = rng.standard_normal((M, K)).astype(np.float32)
+    xt = rng.standard_normal((N, K))
+    monkeypatch.setenv("RGSV_TF32_2SM", "1")
+    y2, _ = _gx(rg, g32, xt, M, N, K)
+    monkeypatch.delenv("RGSV_TF32_2SM")
+    y1, _ = _gx(rg, g32, xt, M, N, K)
+    ref = g32.astype(np.float64) @ xt.T
+    assert np.linalg.norm(y2 - ref) <= 2e-6 * np.linalg.norm(ref)
+    assert np.linalg.norm(y2 - y1) <= 1e-6 * np.linalg.norm(ref)
