@@ -183,6 +183,11 @@ class _Ops:
         return float(out.item())
 
 
+# smallest |R_jj| / max |R_jj| a block may have and still take CholeskyQR3
+# (RGSV_CHOLQR_COND overrides; the one-CTA Householder fallback is ~100x slower)
+RGSV_CHOLQR_COND = float(os.environ.get("RGSV_CHOLQR_COND", "1e-13"))
+
+
 def _block_qr(ops: _Ops, y, m: int, w: int, wp: int, trim_cut: float):
     """reduced_qr of one sketch block with the reference's phase (core.py:80-95)
     and |diag R| for the trim test. Well-conditioned blocks take shifted
@@ -198,8 +203,11 @@ def _block_qr(ops: _Ops, y, m: int, w: int, wp: int, trim_cut: float):
         ops.gtq(_dev.vp(q), wp, _dev.vp(y), wp, _dev.vp(r), wp, wp, wp, m)
         rd = torch.diagonal(r)[:w].abs().cpu().numpy()
         ok = (int(ops.status.item()) & (ST_CHOL | ST_NONFINITE)) == 0
+        # shifted CholeskyQR3 is backward stable up to cond ~ 1/u (Fukaya et
+        # al. 2020), so only blocks near the trim threshold or beyond that
+        # conditioning need Householder's rank-revealing diagonal
         if ok and np.all(np.isfinite(rd)) and rd.min() >= max(1e3 * trim_cut,
-                                                               1e-8 * rd.max()):
+                                                               RGSV_CHOLQR_COND * rd.max()):
             return q, rd
     q, rd = ops.householder(y, m, w, wp)
     return q, rd.cpu().numpy()
