@@ -206,9 +206,14 @@ def _block_qr(ops: _Ops, y, m: int, w: int, wp: int, trim_cut: float):
         # shifted CholeskyQR3 is backward stable up to cond ~ 1/u (Fukaya et
         # al. 2020), so only blocks near the trim threshold or beyond that
         # conditioning need Householder's rank-revealing diagonal
-        if ok and np.all(np.isfinite(rd)) and rd.min() >= max(1e3 * trim_cut,
-                                                               RGSV_CHOLQR_COND * rd.max()):
-            return q, rd
+        # the trim decision (|R_jj| >= trim_cut) must match Householder's: the
+        # CholeskyQR diagonal agrees with it to ~cond * u relative, so a block
+        # whose smallest |R_jj| clears the cut by a condition-scaled margin
+        # (1e-10 * max/min, i.e. >= 1e6 u * cond) decides the same way
+        if ok and np.all(np.isfinite(rd)) and rd.min() > 0.0:
+            margin = 1.0 + 1e-10 * rd.max() / rd.min()
+            if rd.min() >= max(margin * trim_cut, RGSV_CHOLQR_COND * rd.max()):
+                return q, rd
     q, rd = ops.householder(y, m, w, wp)
     return q, rd.cpu().numpy()
 

@@ -12,7 +12,7 @@ from oracle import rgsv_oracle as orc  # noqa: E402
 from paper_2404_09459_b200.workloads import CONFIGS, make_pair  # noqa: E402
 
 np.set_printoptions(precision=4, linewidth=150)
-cfg = CONFIGS["cfg0"]
+cfg = CONFIGS[os.environ.get("CFG", "cfg0")]
 g1, g2 = make_pair(cfg)
 pair = rg.GmpPair(g1, g2)
 run = rg.engine.run_device_pipeline(pair, rg.GsvOptions())
