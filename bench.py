@@ -128,6 +128,7 @@ def cpu_baseline(cfg, budget_s: float, g1, g2):
     """Oracle restatement on the host cores, bounded sample of whole pairs."""
     from oracle import rgsv_oracle as orc
 
+    threads = _all_blas_threads()
     t_start = time.perf_counter()
     done = 0
     while True:
@@ -136,10 +137,10 @@ def cpu_baseline(cfg, budget_s: float, g1, g2):
         if time.perf_counter() - t_start > budget_s or done >= 50:
             break
     dt = time.perf_counter() - t_start
-    return {"value": done / dt, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "port",
+    return {"value": done / dt, "unit": "pairs/s", "cores": threads, "kind": "port",
             "sample": f"{done} whole {cfg.name} pairs (k={cfg.k}, q={cfg.q}) through "
                       f"oracle/rgsv_oracle.run_pipeline, numpy {__import__('numpy').__version__}"
-                      f" + OpenBLAS on {os.cpu_count()} host threads, {dt:.1f} s"}
+                      f" + OpenBLAS on {threads} host threads, {dt:.1f} s"}
 
 
 def workload_desc(cfg):
@@ -148,11 +149,26 @@ def workload_desc(cfg):
             f"q={cfg.q}, fixed-rank range finder, Omega seed = step index")
 
 
+def _all_blas_threads() -> int:
+    """Let the host BLAS use every core (torchrun exports OMP_NUM_THREADS=1
+    to its workers); returns the thread count in effect."""
+    n = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+
+        threadpool_limits(limits=n, user_api="blas")
+        got = [p.get("num_threads", n) for p in threadpool_info() if p.get("user_api") == "blas"]
+        return max(got) if got else n
+    except Exception:  # threadpoolctl missing: report the env setting
+        return int(os.environ.get("OPENBLAS_NUM_THREADS", os.environ.get("OMP_NUM_THREADS", n)))
+
+
 def run_reference(args, rank, world):
     from paper_2404_09459_b200.workloads import CONFIGS, make_pair
 
     if rank != 0:
         return
+    threads = _all_blas_threads()
     cfg = CONFIGS[args.config]
     g1, g2 = make_pair(cfg)
     from oracle import rgsv_oracle as orc
@@ -170,11 +186,12 @@ def run_reference(args, rank, world):
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(cfg), "parallelism": "host cores"},
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": os.cpu_count(),
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{args.steps} whole pairs through the numpy restatement of "
                                    "the reference (oracle/rgsv_oracle.py; the reference has no "
-                                   "power iteration, SURVEY.md §0 F1)"},
+                                   f"power iteration, SURVEY.md §0 F1), OpenBLAS on {threads} "
+                                   "host threads"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -814,6 +831,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
+        # every host core for the CPU reference: torchrun exports
+        # OMP_NUM_THREADS=1, under which a threaded OpenBLAS runs its whole
+        # thread team on one OpenMP thread (slower than one thread); set it
+        # before numpy / OpenBLAS load
+        ncpu = str(os.cpu_count() or 1)
+        os.environ["OMP_NUM_THREADS"] = ncpu
+        os.environ["OPENBLAS_NUM_THREADS"] = ncpu
         run_reference(args, rank, world)
         return
     import torch
