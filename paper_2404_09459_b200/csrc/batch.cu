@@ -27,7 +27,7 @@ namespace {
 // g_batch_prof[phase]. Off in the product build.
 #ifdef RGSV_BATCH_PROFILE
 }  // namespace
-__device__ unsigned long long g_batch_prof[16];
+__device__ unsigned long long g_batch_prof[24];
 namespace {
 #define PROF_T0() long long _pt = clock64()
 #define PROF(ph)                                                                  \
@@ -388,6 +388,9 @@ struct Chain {
       return;
     }
     if (warp == 0) {
+#ifdef RGSV_BATCH_PROFILE
+      long long _g0 = clock64();
+#endif
       const bool row_ok = lane < k;
       double a[KP], x[KP];
 #pragma unroll
@@ -407,6 +410,9 @@ struct Chain {
           if (c == lane && row_ok) a[c] += sh;
       }
       bool bad = false;
+#ifdef RGSV_BATCH_PROFILE
+      long long _g1 = clock64();
+#endif
 #pragma unroll
       for (int j = 0; j < KP; ++j) {
         const double d = __shfl_sync(0xffffffffu, a[j], j);
@@ -429,12 +435,24 @@ struct Chain {
         }
         a[j] = (lane > j) ? 0.0 : (lane == j ? d * r : a[j]);
       }
+#ifdef RGSV_BATCH_PROFILE
+      long long _g2 = clock64();
+#endif
       if (bad) fail = 1;
       if (lane < KP) {
 #pragma unroll
         for (int c = 0; c < KP; ++c)
           linv[lane * LD + c] = bad ? (lane == c ? 1.0 : 0.0) : (c <= lane ? x[c] : 0.0);
       }
+#ifdef RGSV_BATCH_PROFILE
+      if (lane == 0 && (blockIdx.x & 3) == 0) {
+        long long _g3 = clock64();
+        atomicAdd(&g_batch_prof[16], (unsigned long long)(_g1 - _g0));
+        atomicAdd(&g_batch_prof[17], (unsigned long long)(_g2 - _g1));
+        atomicAdd(&g_batch_prof[18], (unsigned long long)(_g3 - _g2));
+        atomicAdd(&g_batch_prof[19], 1ull);
+      }
+#endif
     }
     __syncthreads();
   }
@@ -757,11 +775,11 @@ int batch_chain(const BatchMat* mats, int nmat, int max_rows, int n, int k, int 
 
 extern "C" int rgsv_debug_batch_profile(unsigned long long* out16, int reset) {
 #ifdef RGSV_BATCH_PROFILE
-  if (out16 && cudaMemcpyFromSymbol(out16, rgsv::g_batch_prof, sizeof(unsigned long long) * 16) !=
+  if (out16 && cudaMemcpyFromSymbol(out16, rgsv::g_batch_prof, sizeof(unsigned long long) * 24) !=
                    cudaSuccess)
     return RGSV_ERR_CUDA;
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[24] = {};
     if (cudaMemcpyToSymbol(rgsv::g_batch_prof, z, sizeof(z)) != cudaSuccess) return RGSV_ERR_CUDA;
   }
   return 0;

@@ -34,7 +34,7 @@ plan.set_seeds([2 * j for j in range(B)])
 plan.launch(cfg.q, 1e-10)
 torch.cuda.synchronize()
 L = rg._native.lib()
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 24)()
 L.rgsv_debug_batch_profile(buf, 1)
 plan.launch(cfg.q, 1e-10)
 torch.cuda.synchronize()
@@ -50,3 +50,7 @@ print(f"total {tot / nm / 4 / 1.9e3:.1f} us per matrix-chain per CTA (clock ~1.9
 print(f"chol calls {buf[15]}, near-identity fast path {buf[14]} "
       f"({buf[13] / max(buf[14], 1) / 1.9e3:.2f} us each incl. the check); "
       f"all chol phases {buf[6] / max(buf[15], 1) / 1.9e3:.2f} us per call")
+
+print(f"shifted Gauss-Jordan (warp 0, per call): load+shift {buf[16] / max(buf[19], 1) / 1.9e3:.2f} us, "
+      f"j-loop {buf[17] / max(buf[19], 1) / 1.9e3:.2f} us, store {buf[18] / max(buf[19], 1) / 1.9e3:.2f} us "
+      f"({buf[19]} calls sampled)")
