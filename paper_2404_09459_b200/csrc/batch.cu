@@ -44,7 +44,7 @@ namespace {
 #endif
 
 constexpr int kTR = 32;       // G rows per streamed tile
-constexpr int kStages = 3;    // cp.async ring depth
+constexpr int kStages = 3;    // cp.async ring depth (4 measured 79.6k vs 81.6k pairs/s at cfg3)
 constexpr int kThreads = 256; // 8 warps
 constexpr int kWarps = kThreads / 32;
 
