@@ -22,6 +22,11 @@ cpu_baseline: the CPU oracle (numpy restatement of the reference with the
          q power iterations; OpenBLAS on the host cores) on a bounded sample.
 N > 1 : one process per GPU, each rank an independent replica pair (the
          pairs are independent), timed as the max over ranks ("weak").
+--sharded: ONE pair per step row-sharded over the ranks (dist.py: NCCL
+         all-reduce of the Gram / Z / B partials), "strong" scaling; cfg2
+         (fp64 DMMA) and cfg4 (fp32, 3xTF32 tensor cores).
+cfg4   : fp32 pairs run the G passes on the tcgen05 tensor cores (3xTF32);
+         the roofline is against 3xTF32 = measured bf16 burst / 2 / 3.
 """
 
 from __future__ import annotations
