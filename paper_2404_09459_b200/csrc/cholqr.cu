@@ -14,8 +14,6 @@
 #include <math.h>
 #include <stdlib.h>
 
-#include <map>
-#include <mutex>
 
 #include "common.cuh"
 #include "rgsv_internal.h"
@@ -910,28 +908,24 @@ __global__ void k_identity2(double* __restrict__ a, double* __restrict__ b, int 
 
 namespace {
 
-struct BlkScratch {
-  double* base = nullptr;
-  size_t bytes = 0;
-};
-
-// One scratch area per stream (kp <= 1024 needs ~4 kp^2 + 10 * 128^2 doubles).
-double* blk_scratch(cudaStream_t st, size_t need) {
-  static std::mutex mu;
-  static std::map<cudaStream_t, BlkScratch> pool;
-  std::lock_guard<std::mutex> lock(mu);
-  BlkScratch& b = pool[st];
-  if (b.bytes < need) {
-    if (b.base) {
-      cudaStreamSynchronize(st);
-      cudaFree(b.base);
+// Scratch of the blocked factorisation: stream-ordered (cudaMallocAsync /
+// cudaFreeAsync), so the call is also capturable in a CUDA graph (memory
+// alloc/free nodes) and concurrent chains on different streams never share
+// it. The default pool keeps freed blocks cached (release threshold max).
+double* blk_scratch_alloc(cudaStream_t st, size_t bytes) {
+  static bool pool_set = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    b.base = nullptr;
-    b.bytes = 0;
-    if (cudaMalloc(&b.base, need) != cudaSuccess) return nullptr;
-    b.bytes = need;
-  }
-  return b.base;
+    return true;
+  }();
+  (void)pool_set;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) return nullptr;
+  return static_cast<double*>(p);
 }
 
 int gemm_small(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
@@ -972,8 +966,13 @@ int chol_inv_blocked(const double* gram, int k, int kp, int64_t shift_rows, doub
   const int nb = (kp + 127) / 128;
   const int bs = ((kp + nb - 1) / nb + 15) / 16 * 16;  // block size, multiple of 16, <= 128
   const size_t kk = (size_t)kp * kp, bb = (size_t)128 * 128;
-  double* base = blk_scratch(st, (4 * kk + (4 + (size_t)nb) * bb + 8 * 128) * sizeof(double));
+  double* base = blk_scratch_alloc(st, (4 * kk + (4 + (size_t)nb) * bb + 8 * 128) * sizeof(double));
   if (!base) return RGSV_ERR_CUDA;
+  struct Release {  // freed in stream order on every exit path
+    double* p;
+    cudaStream_t s;
+    ~Release() { cudaFreeAsync(p, s); }
+  } release{base, st};
   double* W = base;            // working copy; lower part becomes L
   double* X = W + kk;          // L^{-1}
   double* T = X + kk;          // GEMM outputs (<= kp x kp)

@@ -315,10 +315,18 @@ def _promoted(pair: GmpPair) -> GmpPair:
     return p64
 
 
+# widest sketch the fused single-call chain (rgsv_sketch_project: its sketch
+# GEMM carries the fused ||G||^2, N <= 128) serves; wider fixed-rank sketches
+# run the same chain as separate launches (rangefinder.chunked_chain)
+_FUSED_MAX_K = 128
+
+
 def _streamed_run(pair: GmpPair, opts: GsvOptions, k1: int, k2: int) -> DeviceRun:
-    """Fixed-rank pipeline for fp32-resident pairs (cfg4): both chains stream
-    G in fp64-promoted row chunks (rangefinder.chunked_chain), then the
-    shared small-GSVD + comparative stage."""
+    """Fixed-rank pipeline as separate launches, matrix by matrix: fp32 pairs
+    (cfg4) take the tf32x3 tensor-core chain (tf32.tf32_chain) or the
+    fp64-promoted row chunks (rangefinder.chunked_chain, f32_mode="promote");
+    fp64 pairs wider than the fused chain (k > 128) take chunked_chain on the
+    resident matrix. Then the shared small-GSVD + comparative stage."""
     cfg = opts.extraction
     lo = None
     res = []
@@ -354,7 +362,7 @@ def run_device_pipeline(pair: GmpPair, opts: GsvOptions, *, sync: bool = True) -
     f32 = pair.g1.is_f32 or pair.g2.is_f32
     if widths is None:
         return _general_run(_promoted(pair) if f32 else pair, opts)
-    if f32:
+    if f32 or max(widths) > _FUSED_MAX_K:
         return _streamed_run(pair, opts, *widths)
     k1, k2 = widths
     plan = _dev.pair_plan(pair.m, pair.p, pair.n, k1, k2)
@@ -439,7 +447,9 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
     if _is_host_pair(pairs[0]):
         return run_host_batch(pairs, opts, seeds)
     first = pairs[0]
-    if any(pr.g1.is_f32 or pr.g2.is_f32 for pr in pairs):  # streamed fp32 pairs, one by one
+    w0 = _fixed_width(opts, first.m, first.p, first.n)
+    if any(pr.g1.is_f32 or pr.g2.is_f32 for pr in pairs) or (
+            w0 is not None and max(w0) > _FUSED_MAX_K):  # chained passes, pair by pair
         cfg0 = opts.extraction
         seeds = [cfg0.seed] * len(pairs) if seeds is None else list(seeds)
         return [run_device_pipeline(pr, dataclasses.replace(

@@ -253,3 +253,24 @@ def test_rank_check_wide_blocked_cholesky():
     g2[:, -1] = g2[:, 0] + g2[:, 1]
     with pytest.raises(rg.RankDeficiencyError):
         rg.GmpPair(g1, g2, check_rank=True)
+
+
+def test_fixed_rank_wide_k():
+    """k = 200 (kp = 208 > 128, beyond the fused single-call chain): the pair
+    runs the chain as separate launches with every CholeskyQR through the
+    blocked Cholesky (stream-ordered scratch), single and batched, and
+    matches the oracle."""
+    cfg = CONFIGS["cfg0"]
+    g1, g2 = make_pair(cfg, data_seed=5, m=3000, p=2500, n=500)
+    pair = rg.GmpPair(g1, g2, check_rank=False)
+    opts = fixed_opts(200, 1, 4)
+    reps = [rg.compare(pair, opts) for _ in range(3)]
+    o = orc.run_pipeline(g1, g2, k=200, q=1, seed=4)
+    for rep in reps:
+        assert np.array_equal(rep.spectrum.alphas, o.alphas)
+        assert (rep.spectrum.r, rep.spectrum.s) == (o.r, o.s)
+        assert np.array_equal(rep.theta, reps[0].theta)
+    pairs = [pair, rg.GmpPair(*make_pair(cfg, data_seed=6, m=3000, p=2500, n=500),
+                              check_rank=False)]
+    out = rg.compare_batch(pairs, opts, seeds=[4, 9])
+    assert np.array_equal(out[0].spectrum.alphas, o.alphas)
