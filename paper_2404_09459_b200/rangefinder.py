@@ -370,6 +370,19 @@ def extract_basis(g, cfg: ExtractionConfig | None = None, *, device_result: bool
         q, _, res = adaptive_device(a, cfg)
         res.q = q if device_result else q.cpu().numpy()
         return res
+    if width > 128:  # beyond the fused call's sketch (N <= 128): separate launches
+        gf2 = _dev.device_sumsq(a)
+        if not math.isfinite(gf2):
+            raise ValidationError("g contains non-finite entries")
+        normf = math.sqrt(gf2)
+        tol = cfg.tol if cfg.tol is not None else 1e-10 * normf
+        if normf == 0.0 or normf < tol:  # rangefinder.py:96
+            q0 = torch.zeros((m, 0), dtype=torch.float64, device="cuda")
+            return BasisResult(q0 if device_result else q0.cpu().numpy(), [normf], True, 0, [])
+        q, _, hist = chunked_chain(a, width, cfg.power_iters, cfg.seed)
+        q = q[:, :width]
+        return BasisResult(q if device_result else q.cpu().numpy(), hist, hist[-1] < tol, 1,
+                           [width])
     plan = _dev.SketchPlan(m, n, width)
     stats = torch.zeros(2, dtype=torch.float64, device="cuda")
     rdiag = torch.zeros(max(width, 1), dtype=torch.float64, device="cuda")

@@ -274,3 +274,24 @@ def test_fixed_rank_wide_k():
                               check_rank=False)]
     out = rg.compare_batch(pairs, opts, seeds=[4, 9])
     assert np.array_equal(out[0].spectrum.alphas, o.alphas)
+
+
+def test_extract_basis_wide_fixed_width():
+    """extract_basis with a fixed width of 200 (> the fused call's 128):
+    same basis contract as the reference (rangefinder.py:68-135)."""
+    cfg = CONFIGS["cfg0"]
+    g1, _ = make_pair(cfg, data_seed=8, m=2500, p=10, n=400)
+    ext = rg.ExtractionConfig.fixed_rank(200, 3, 1)
+    res = rg.extract_basis(g1, ext)
+    ob = orc.fixed_rank_basis(g1, 200, 1, 3)
+    assert res.q.shape == (2500, 200) and res.block_widths == [200]
+    assert np.linalg.norm(res.q.T @ res.q - np.eye(200)) <= 1e-12 * np.sqrt(200)
+    assert abs(res.residual_history[0] - ob.residual_history[0]) <= 1e-13 * ob.residual_history[0]
+    e = res.residual_history[0] ** 2 - res.residual_history[1] ** 2
+    eo = orc.sum_sq(ob.b)
+    assert abs(e - eo) <= 1e-12 * eo
+    s = cfg.s
+    qa, _ = np.linalg.qr(res.q[:, :s])
+    qb, _ = np.linalg.qr(ob.q[:, :s])
+    # sine of the largest principal angle (arccos is blind below ~1e-8)
+    assert np.linalg.norm(qb - qa @ (qa.T @ qb), 2) <= 1e-10
