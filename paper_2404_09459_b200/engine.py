@@ -406,6 +406,10 @@ def _is_host_pair(pr) -> bool:
     return not isinstance(pr, GmpPair)
 
 
+def _is_f32_host(a) -> bool:
+    return getattr(a, "dtype", None) in (np.float32, torch.float32)
+
+
 def run_host_batch(host_pairs, opts: GsvOptions, seeds=None) -> list:
     """B pairs given as (g1, g2) HOST arrays (numpy or torch CPU tensors,
     pinned for full speed): streamed to the device with every pair's
@@ -428,8 +432,13 @@ def run_host_batch(host_pairs, opts: GsvOptions, seeds=None) -> list:
     if len(seeds) != len(host_pairs):
         raise DimensionError("one seed per pair")
     widths = _fixed_width(opts, m, p, n)
-    if widths is None:
-        pairs = [GmpPair(a, b) for a, b in host_pairs]
+    f32 = opts.f32_mode == "tf32x3" and any(_is_f32_host(a) or _is_f32_host(b)
+                                             for a, b in host_pairs)
+    if widths is None or f32 or max(widths) > _FUSED_MAX_K:
+        # general modes, fp32 pairs (tensor-core chain) and wide sketches:
+        # upload and run pair by pair
+        pairs = [GmpPair(a, b, check_rank=False if widths is not None else None)
+                 for a, b in host_pairs]
         return run_device_batch(pairs, opts, seeds)
     k1, k2 = widths
     plan = _dev.host_stream_plan(len(host_pairs), m, p, n, k1, k2)

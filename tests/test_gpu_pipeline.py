@@ -295,3 +295,14 @@ def test_extract_basis_wide_fixed_width():
     qb, _ = np.linalg.qr(ob.q[:, :s])
     # sine of the largest principal angle (arccos is blind below ~1e-8)
     assert np.linalg.norm(qb - qa @ (qa.T @ qb), 2) <= 1e-10
+
+
+def test_host_batch_wide_k():
+    """compare_batch on host pairs with k = 200 (> the fused chain) matches
+    the oracle."""
+    cfg = CONFIGS["cfg0"]
+    hosts = [make_pair(cfg, data_seed=d, m=2200, p=2000, n=450) for d in (11, 12)]
+    reps = rg.compare_batch(hosts, fixed_opts(200, 1, 0), seeds=[2, 3])
+    for (g1, g2), rep, sd in zip(hosts, reps, (2, 3)):
+        o = orc.run_pipeline(g1, g2, k=200, q=1, seed=sd)
+        assert np.array_equal(rep.spectrum.alphas, o.alphas)

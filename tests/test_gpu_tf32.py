@@ -255,3 +255,18 @@ def test_gx_cta_pair_variant(rg, M, N, K, monkeypatch):
     ref = g32.astype(np.float64) @ xt.T
     assert np.linalg.norm(y2 - ref) <= 2e-6 * np.linalg.norm(ref)
     assert np.linalg.norm(y2 - y1) <= 1e-6 * np.linalg.norm(ref)
+
+
+def test_host_batch_fp32_takes_tensor_core_chain(rg):
+    """compare_batch on fp32 HOST pairs runs the tf32x3 chain (default
+    f32_mode) pair by pair, and its reports equal the single-pair calls."""
+    pairs = [_f32_pair(m=1500, p=1200, n=256, seed=s) for s in (1, 2)]
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(32, 0, 1))
+    reps = rg.compare_batch(pairs, opts, seeds=[3, 4])
+    for (g1, g2), rep, sd in zip(pairs, reps, (3, 4)):
+        single = rg.compare(rg.GmpPair(g1, g2, check_rank=False),
+                            rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(32, sd, 1)))
+        assert np.array_equal(rep.spectrum.alphas, single.spectrum.alphas)
+        assert np.array_equal(rep.theta, single.theta) and rep.d1 == single.d1
+        o = orc.run_pipeline(g1.astype(np.float64), g2.astype(np.float64), k=32, q=1, seed=sd)
+        assert (rep.spectrum.r, rep.spectrum.s) == (o.r, o.s)
