@@ -40,6 +40,19 @@ def test_argument_errors_are_reported_without_launch():
                                null) == _native.ERR_RANK
     assert lib.rgsv_comparative(null, null, null, 4, 0.5, null, null, null, null, null, null,
                                 null, null, null, null) == _native.ERR_VALIDATION
+    # tf32x3 entry points: N must be a multiple of 32 in [32, 320]; fp32
+    # pitches a multiple of 4 elements; fp64 output pitch even
+    assert lib.rgsv_tf32x3_gx(null, null, 64, null, null, 64, null, 48, 100, 48, 64,
+                              null) == _native.ERR_DIMENSION
+    assert lib.rgsv_tf32x3_gx(null, null, 66, null, null, 64, null, 64, 100, 64, 64,
+                              null) == _native.ERR_DIMENSION
+    assert lib.rgsv_tf32x3_gx(null, null, 64, null, null, 64, null, 352, 100, 352, 64,
+                              null) == _native.ERR_DIMENSION
+    assert lib.rgsv_tf32x3_gtq(null, null, 48, null, null, 64, null, 64, 48, 64, 100, null, 0,
+                               null) == _native.ERR_DIMENSION
+    assert lib.rgsv_f32_split(null, 8, 4, 16, null, 16, 0, null, null, 0,
+                              null) == _native.ERR_DIMENSION
+    assert lib.rgsv_f64_split_tf32(null, 8, 4, 8, null, null, 4, 4, null) == _native.ERR_DIMENSION
 
 
 def test_error_mapping():
