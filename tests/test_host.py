@@ -228,3 +228,24 @@ def test_sharded_bench_mode_is_wired():
         m = CONFIGS[cfg].m
         blocks = [rdist.shard_rows(m, r, 8) for r in range(8)]
         assert blocks[0][0] == 0 and blocks[-1][1] == m
+
+
+def test_projector_bound_host_formula_matches_reference_golden():
+    """projector_bound is O(n) host math on top of the device-validated
+    stacked norm: with the reference's own stack_norm2 and spectrum it
+    reproduces the reference's certificates (tests/golden/ref_bounds.npz)."""
+    import os
+    from types import SimpleNamespace
+
+    from paper_2404_09459_b200.bounds import projector_bound
+
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_bounds.npz"))
+    for c in (0, 1):
+        g1, g2 = gold[f"c{c}_g1"], gold[f"c{c}_g2"]
+        pair = SimpleNamespace(m=g1.shape[0], p=g2.shape[0], n=g1.shape[1],
+                               stack_norm2=float(gold[f"c{c}_stack_norm2"]))
+        spec = SimpleNamespace(alphas=gold[f"c{c}_alphas"], betas=gold[f"c{c}_betas"])
+        for k, os_, side, want in gold[f"c{c}_projector"]:
+            got = projector_bound(pair, spec, k=int(k), oversample=int(os_),
+                                  which="first" if side == 0 else "second")
+            assert got == want or abs(got - want) <= 1e-14 * abs(want)
