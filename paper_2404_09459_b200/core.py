@@ -17,7 +17,7 @@ import torch
 
 from . import device as _dev
 from ._native import check, lib
-from .errors import DimensionError, ValidationError
+from .errors import ConvergenceError, DimensionError, RankDeficiencyError, ValidationError
 
 REAL = "real"
 COMPLEX = "complex"
@@ -129,3 +129,57 @@ def _qr_in_place(y: torch.Tensor, rows: int, k: int) -> torch.Tensor:
 
 __all__ = ["REAL", "COMPLEX", "QrFactors", "SvdFactors", "as_matrix", "gaussian_matrix",
            "sum_sq", "frobenius_norm", "reduced_qr"]
+
+
+def svd(m) -> SvdFactors:
+    """Reduced SVD (core.py:99-106) on the device: one-sided Jacobi with
+    accumulated rotations (rgsv_svd_vectors), orthonormal completion for
+    exactly-zero singular values; ``u @ diag(s) @ v.T`` reconstructs the
+    input, ``s`` nonincreasing. Non-convergence raises ConvergenceError
+    (the reference's LinAlgError mapping)."""
+    from .recovery import _buf, _Dense
+
+    g = as_matrix(m)
+    rows, cols = g.rows, g.cols
+    if min(rows, cols) > 2048:
+        raise DimensionError("B200 svd supports min(rows, cols) <= 2048 (one-sided Jacobi)")
+    blk = _buf(rows, cols)
+    blk[:rows, :cols] = g.t
+    dense = _Dense()
+    u, vh = dense.svd_full(blk, rows, cols)
+    r = min(rows, cols)
+    s = dense.last_sv[:r]
+    if rows <= cols:
+        u_red, v_red = u[:rows, :r], vh[:r, :cols].T
+    else:
+        u_red, v_red = u[:rows, :r], vh[:cols, :cols].T
+    return SvdFactors(u_red.cpu().numpy(), s.cpu().numpy(), v_red.cpu().numpy())
+
+
+def pseudoinverse_norm(m) -> float:
+    """1 / sigma_min for a matrix of full column rank (core.py:133-150);
+    singular values from the device Jacobi. RankDeficiencyError otherwise."""
+    from .validation import _jacobi_values
+
+    g = as_matrix(m)
+    rows, cols = g.rows, g.cols
+    if rows < cols:
+        raise RankDeficiencyError(f"matrix of shape {(rows, cols)} cannot have full column rank")
+    a = torch.zeros((rows, cols + (cols & 1)), dtype=torch.float64, device="cuda")
+    a[:, :cols] = g.t
+    try:
+        sv = _jacobi_values(a, rows, cols)
+    except ConvergenceError:
+        # exactly dependent columns can stall the values-only Jacobi; the
+        # CholeskyQR route then reports the rank deficiency like the reference
+        if _dev.ceil16(cols) > 1024:
+            raise
+        y = torch.zeros((rows, _dev.ceil16(cols)), dtype=torch.float64, device="cuda")
+        y[:, :cols] = g.t
+        r = _qr_in_place(y, rows, cols)[:cols, :cols].contiguous()  # raises RankDeficiencyError
+        sv = _jacobi_values(r, cols, cols)
+    smax, smin = float(sv[0]), float(sv[-1])
+    if smin <= 1e-13 * smax:
+        raise RankDeficiencyError(f"smallest singular value {smin:.3e} below rank threshold "
+                                  f"{1e-13 * smax:.3e}")
+    return 1.0 / smin

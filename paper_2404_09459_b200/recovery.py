@@ -122,6 +122,7 @@ class _Dense:
         code, nzero = (int(x) for x in status[:2].cpu().tolist())
         if code & ST_JACOBI:
             raise ConvergenceError("Jacobi SVD of an L block did not converge")
+        self.last_sv = sv  # descending singular values (core.svd reads them)
         if rows <= n:
             u = self.tr(jo, nv, nv)                      # U = Jᵀ (rows x rows)
             vh = _buf(n, n)

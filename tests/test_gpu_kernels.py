@@ -198,3 +198,31 @@ def test_chol_inv_near_identity_path(k, scale):
     assert np.array_equal(li[k:, k:], np.eye(kp - k)) and not np.any(li[:k, k:])
     assert np.max(np.abs(rd.cpu().numpy()[:k] - np.diag(np.linalg.cholesky(a)))) <= 1e-15
     assert np.array_equal(rinv.cpu().numpy(), li.T)
+
+
+@pytest.mark.parametrize("rows,cols", [(60, 20), (20, 60), (128, 128), (300, 37)])
+def test_core_svd_and_pseudoinverse_norm(rows, cols):
+    """core.svd / core.pseudoinverse_norm (core.py:99-150) on the device
+    Jacobi: reconstruction, orthonormal factors, LAPACK's singular values."""
+    import paper_2404_09459_b200 as rg
+
+    a = np.random.default_rng(rows * cols).standard_normal((rows, cols))
+    f = rg.svd(a)
+    r = min(rows, cols)
+    assert f.u.shape == (rows, r) and f.s.shape == (r,) and f.v.shape == (cols, r)
+    assert np.linalg.norm(f.u @ np.diag(f.s) @ f.v.T - a) <= 1e-12 * np.linalg.norm(a)
+    assert np.linalg.norm(f.u.T @ f.u - np.eye(r)) <= 1e-12 * np.sqrt(r)
+    assert np.linalg.norm(f.v.T @ f.v - np.eye(r)) <= 1e-12 * np.sqrt(r)
+    s_ref = np.linalg.svd(a, compute_uv=False)
+    assert np.max(np.abs(f.s - s_ref)) <= 1e-12 * s_ref[0]
+    assert np.all(np.diff(f.s) <= 0)
+    if rows >= cols:
+        assert abs(rg.pseudoinverse_norm(a) - 1 / s_ref[-1]) <= 1e-10 / s_ref[-1]
+    else:
+        with pytest.raises(rg.RankDeficiencyError):
+            rg.pseudoinverse_norm(a)
+    b = a.copy()
+    if rows >= cols:
+        b[:, -1] = b[:, 0]
+        with pytest.raises(rg.RankDeficiencyError):
+            rg.pseudoinverse_norm(b)
