@@ -326,7 +326,7 @@ def run_ours_batch(args, rank, world):
     d2h = eplan.fhost.numel() * 8 + eplan.ihost.numel() * 4
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         hg1, hg2 = make_pair(cfg, data_seed=0)
         cpu = cpu_baseline(cfg, args.cpu_sample_seconds, hg1, hg2)
     if rank == 0:
@@ -495,7 +495,7 @@ def run_ours_f32(args, rank, world):
     e2e_value = ne / (e0.elapsed_time(e1) * 1e-3)
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         # oracle on a 1/50-row fp64 instance, extrapolated linearly in rows
         ms, ps = cfg.m // 50, cfg.p // 50
         hg1, hg2 = make_pair(cfg, data_seed=0, m=ms, p=ps)
@@ -786,7 +786,7 @@ def run_ours(args, rank, world):
             traffic = None
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline and world >= 1:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         cpu = cpu_baseline(cfg, args.cpu_sample_seconds, g1h, g2h)
 
     if rank == 0:
