@@ -214,7 +214,7 @@ def test_f32_row_sharded_chain_two_shards(rg):
     assert abs(out[0][2][0] - h_ref[0]) <= 1e-13 * h_ref[0]
 
 
-@pytest.mark.parametrize("m,p,n,k,q", [(300, 200, 64, 16, 1), (1000, 900, 301, 20, 1),
+@pytest.mark.parametrize("m,p,n,k,q", [(300, 200, 64, 16, 1), (1000, 900, 301, 20, 1), (50, 70, 40, 8, 1),
                                        (129, 150, 100, 40, 0), (2000, 1500, 256, 100, 2)])
 def test_tf32_pair_edge_shapes(rg, m, p, n, k, q):
     """kp not a multiple of 32 (zero-padded tensor-core operands), odd n
