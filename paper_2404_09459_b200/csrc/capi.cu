@@ -102,6 +102,17 @@ static int proj_split() {
   }();
   return v;
 }
+// Split cap of the tail tiles of the G X passes (RGSV_GX_SPLIT; tuning).
+// cfg1 with 8 concurrent pairs: 713 / 720 / 720 pairs/s at 32 / 4 / 1 and
+// 2.30 / 2.35 / 2.41 ms single-pair latency.
+static int gx_split() {
+  static const int v = [] {
+    const char* e = getenv("RGSV_GX_SPLIT");
+    const int x = e ? atoi(e) : 0;
+    return x >= 1 ? x : 4;
+  }();
+  return v;
+}
 constexpr int kIntermediatePasses = 3;  // see the note in rgsv_sketch_project
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -344,7 +355,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
   s.K = n;
   s.scratch = scratch;
   s.scratch_bytes = sb;
-  s.max_split = 32;
+  s.max_split = gx_split();
   s.ss_out = ss;
   int ss_units = 0;
   s.ss_units = &ss_units;
