@@ -1164,6 +1164,24 @@ int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram,
   return 0;
 }
 
+// Split caps of the wide CholeskyQR3's Gram (which = 0, RGSV_WGRAM_SPLIT) and
+// TRSM (which = 1, RGSV_WTRSM_SPLIT). cfg1 with 8 concurrent pairs (n = 1000,
+// kp = 64): 713-720 pairs/s at 32 / 8, 720-723 at 16 / 2 and 8 / 2,
+// 725-733 at 8 / 1 (fewer partials and no reduce pass for the TRSM).
+static int wide_split(int which) {
+  static const int v[2] = {[] {
+                             const char* e = getenv("RGSV_WGRAM_SPLIT");
+                             const int x = e ? atoi(e) : 0;
+                             return x >= 1 ? x : 8;
+                           }(),
+                           [] {
+                             const char* e = getenv("RGSV_WTRSM_SPLIT");
+                             const int x = e ? atoi(e) : 0;
+                             return x >= 1 ? x : 1;
+                           }()};
+  return v[which];
+}
+
 int cholqr3_wide(double* b, double* tmp, int64_t n, int64_t ldn, int k, int kp, double* gram,
                  double* linv, double* rinv, double* rdiag, double* scratch, size_t scratch_bytes,
                  int* status, double** qt_out, cudaStream_t st, int passes) {
@@ -1182,7 +1200,7 @@ int cholqr3_wide(double* b, double* tmp, int64_t n, int64_t ldn, int k, int kp, 
     g.K = n;
     g.scratch = scratch;
     g.scratch_bytes = scratch_bytes;
-    g.max_split = 32;
+    g.max_split = wide_split(0);
     if (int e = gemm_gx(g, st)) return e;
     if (int e = chol_inv(gram, k, kp, step == 0 ? n : 0, linv, rinv, nullptr,
                          step == 0 ? rdiag : nullptr, step == 0 ? nullptr : rdiag, status, st))
@@ -1199,7 +1217,7 @@ int cholqr3_wide(double* b, double* tmp, int64_t n, int64_t ldn, int k, int kp, 
     t.K = kp;
     t.scratch = scratch;
     t.scratch_bytes = scratch_bytes;
-    t.max_split = 8;
+    t.max_split = wide_split(1);
     if (int e = gemm_gtq(t, st)) return e;
     double* sw = src;
     src = dst;
