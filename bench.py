@@ -4,10 +4,11 @@
     python bench.py [--gpus N --steps K --warmup W] [--config cfg1] [--impl reference]
 
 A step is one full randomized GSVD + comparative analysis of a batch of B
-independent matrix pairs (BASELINE.json configs; cfg1 by default: fp64,
-m=20000, p=16000, n=1000, k=60, q=2; B=8 distinct seeded pairs resident in
-HBM) run concurrently through compare_batch, with fresh Ω seeds every step
-(the reference's run_bench convention, bench.py:98-102).
+independent matrix pairs (BASELINE.json configs) run concurrently through
+compare_batch, with fresh Ω seeds every step (the reference's run_bench
+convention, bench.py:98-102). The default workload is cfg2, the config
+BASELINE.json's metric is quoted on ("Throughput reported at 1/2/4/8
+GPUs"): fp64, m=200000, p=150000, n=4000, k=120, q=2, one pair per step.
 latency_ms_per_pair reports one pair at a time through compare(). Synthetic seeded data with the
 config's shape/rank/noise (paper_2404_09459_b200/workloads.py) stands in
 for the paper's genome datasets.
@@ -20,11 +21,15 @@ roofline: the dominant GEMM kernel timed live with CUDA events on its
          issue peak measured on this pool (profiles/r01_fp64_peak.log).
 cpu_baseline: the CPU oracle (numpy restatement of the reference with the
          q power iterations; OpenBLAS on the host cores) on a bounded sample.
-N > 1 : one process per GPU, each rank an independent replica pair (the
-         pairs are independent), timed as the max over ranks ("weak").
---sharded: ONE pair per step row-sharded over the ranks (dist.py: NCCL
-         all-reduce of the Gram / Z / B partials), "strong" scaling; cfg2
-         (fp64 DMMA) and cfg4 (fp32, 3xTF32 tensor cores).
+N > 1 : one process per GPU. Single-pair configs (cfg2, cfg4; cfg0/cfg1
+         with --sharded) run ONE pair per step row-sharded over the ranks
+         (dist.py: NCCL all-reduce of the Gram / Z / B partials), "strong"
+         scaling, as north_star asks; --replicas times independent replica
+         pairs per rank instead ("weak"). cfg3 is always replicas (its pairs
+         are independent).
+metric: the same string in both arms ("rGSVD pairs/sec (cfgN)"), so the
+         driver can pair our line with the reference arm's; the sketch-GEMM
+         TFLOP/s and its roofline fraction are separate keys.
 cfg4   : fp32 pairs run the G passes on the tcgen05 tensor cores (3xTF32);
          the roofline is against 3xTF32 = measured bf16 burst / 2 / 3.
 """
@@ -64,7 +69,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--config", default="cfg2")
     ap.add_argument("--batch", type=int, default=None,
                     help="independent pairs per step, processed concurrently (compare_batch); "
                          "default 8 for cfg0/cfg1 (measured 643/676/686 pairs/s at 4/6/8 on "
@@ -75,8 +80,17 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="ONE pair row-sharded over the ranks (dist.compute_gsv_sharded, NCCL "
-                         "all-reduce of the Gram / Z / B partials): strong scaling, cfg2/cfg4")
+                         "all-reduce of the Gram / Z / B partials): strong scaling; the default "
+                         "at N > 1 for the single-pair configs")
+    ap.add_argument("--replicas", action="store_true",
+                    help="at N > 1: independent replica pairs per rank (weak scaling) instead "
+                         "of one row-sharded pair")
     return ap.parse_args()
+
+
+def metric(cfg) -> str:
+    """The metric string both arms print (identical, so the driver pairs them)."""
+    return f"rGSVD pairs/sec ({cfg.name})"
 
 
 class Clocks:
@@ -169,13 +183,25 @@ def _all_blas_threads() -> int:
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the CPU restatement of the reference path
+    (oracle/rgsv_oracle.run_pipeline: bench._timed_run's region, reference
+    bench.py:72-79, plus the q power iterations the reference lacks) on the
+    same config, whole pairs per step, all host cores. Rank 0 only."""
     from paper_2404_09459_b200.workloads import CONFIGS, make_pair
 
     if rank != 0:
         return
     threads = _all_blas_threads()
     cfg = CONFIGS[args.config]
-    g1, g2 = make_pair(cfg)
+    scale, inst = 1.0, ""
+    if cfg.dtype == "f32":  # cfg4: 118 GB of host fp64; a 1/50-row instance, scaled by rows
+        ms, ps = cfg.m // 50, cfg.p // 50
+        g1, g2 = make_pair(cfg, m=ms, p=ps)
+        scale = (ms + ps) / (cfg.m + cfg.p)
+        inst = (f"; each step one m={ms} p={ps} instance (1/50 of the rows, fp64 as the reference "
+                f"promotes), pairs/s scaled by rows x{scale:.4f}")
+    else:
+        g1, g2 = make_pair(cfg)
     from oracle import rgsv_oracle as orc
 
     for i in range(args.warmup):
@@ -184,9 +210,9 @@ def run_reference(args, rank, world):
     for i in range(args.steps):
         orc.run_pipeline(g1, g2, k=cfg.k, q=cfg.q, seed=i)
     dt = time.perf_counter() - t0
-    value = args.steps / dt
+    value = args.steps / dt * scale
     line = {
-        "impl": "reference", "metric": f"rGSVD pairs/sec ({cfg.name})", "value": value,
+        "impl": "reference", "metric": metric(cfg), "value": value,
         "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -196,11 +222,31 @@ def run_reference(args, rank, world):
                          "sample": f"{args.steps} whole pairs through the numpy restatement of "
                                    "the reference (oracle/rgsv_oracle.py; the reference has no "
                                    f"power iteration, SURVEY.md §0 F1), OpenBLAS on {threads} "
-                                   "host threads"},
+                                   f"host threads{inst}"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def committed_traffic(cfg_name: str, kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of `kernel` at this config's shapes, from the newest committed ncu
+    summary profiles/rNN_gemm_<cfg>_traffic.json (None when there is none)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_*{cfg_name}_traffic.json")),
+                       reverse=True):
+        try:
+            d = json.load(open(path)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            continue
+        if isinstance(d, dict):
+            if kernel in d:
+                return float(d[kernel])
+        elif d is not None and kernel == "k_gtq":  # round-1 format: the gtq launch only
+            return float(d)
+    return None
 
 
 def time_kernel(fn, reps=20):
@@ -332,7 +378,7 @@ def run_ours_batch(args, rank, world):
     if rank == 0:
         rep = reps[0]
         line = {
-            "metric": f"rGSVD pairs/sec ({cfg.name}); sketch-GEMM TFLOP/s (% FP64 TC roofline)",
+            "metric": metric(cfg),
             "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -509,7 +555,7 @@ def run_ours_f32(args, rank, world):
                          "118 GB of host fp64"}
     if rank == 0:
         line = {
-            "metric": f"rGSVD pairs/sec ({cfg.name}); sketch-GEMM TFLOP/s (% FP64 TC roofline)",
+            "metric": metric(cfg),
             "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -620,7 +666,7 @@ def run_ours_sharded(args, rank, world):
         peak = MEASURED_BF16_TFLOPS / 6.0 if f32 else FP64_DMMA_PEAK_TFLOPS
         eff = cfg.flops * value / world / 1e12
         line = {
-            "metric": f"rGSVD pairs/sec ({cfg.name}, one pair row-sharded over {world} GPU)",
+            "metric": metric(cfg),
             "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -777,13 +823,7 @@ def run_ours(args, rank, world):
     gemm_time = per_pair * (t_gtq + t_gx) * (cfg.m + cfg.p) / cfg.m
     sketch_tflops = cfg.flops / gemm_time / 1e12
     step_s = t_max / (args.steps * B)
-    traffic = None  # the committed ncu capture is of the cfg1 gtq launch only
-    prof = os.path.join(ROOT, "profiles", "r01_gtq_cfg1_traffic.json")
-    if cfg.name == "cfg1" and os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
+    traffic = committed_traffic(cfg.name, "k_gtq" if t_gtq >= t_gx else "k_gx")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
@@ -791,7 +831,7 @@ def run_ours(args, rank, world):
 
     if rank == 0:
         line = {
-            "metric": f"rGSVD pairs/sec ({cfg.name}); sketch-GEMM TFLOP/s (% FP64 TC roofline)",
+            "metric": metric(cfg),
             "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "latency_ms_per_pair": latency_ms,
@@ -856,7 +896,7 @@ def main():
 
     if CONFIGS[args.config].batch > 1:
         run_ours_batch(args, rank, world)
-    elif args.sharded:
+    elif args.sharded or (world > 1 and not args.replicas):
         run_ours_sharded(args, rank, world)
     elif CONFIGS[args.config].dtype == "f32":
         run_ours_f32(args, rank, world)

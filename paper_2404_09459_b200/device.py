@@ -307,10 +307,13 @@ class PairPlan:
         self.last_key = None
         self.kernels_per_replay = 0
 
-    def enqueue(self, g1: DevMatrix, g2: DevMatrix, q_iters: int, classify_tol: float) -> None:
+    def enqueue(self, g1: DevMatrix, g2: DevMatrix, q_iters: int, classify_tol: float,
+                ready1=None, ready2=None) -> None:
         """Every device operation of one pair, on the current stream (G1
         chain, small GSVD, comparative kernel, packed D2H) and the side
-        stream (G2 chain). Capturable as one CUDA graph."""
+        stream (G2 chain). Capturable as one CUDA graph. ready1 / ready2:
+        optional events after which G1 / G2 are valid (the end-to-end path
+        starts the G1 chain while G2 is still crossing PCIe)."""
         L = lib()
         main = torch.cuda.current_stream()
         pk = self.pk
@@ -318,6 +321,10 @@ class PairPlan:
         self.side.wait_stream(main)
         self.s1.enqueue_omega(pk.d("status"), main)
         self.s2.enqueue_omega(pk.d("status"), self.side)
+        if ready1 is not None:
+            main.wait_event(ready1)
+        if ready2 is not None:
+            self.side.wait_event(ready2)
         self.s1.launch(g1, q_iters, pk.d("stats1"), pk.d("rdiag1"), pk.d("status"), main)
         self.s2.launch(g2, q_iters, pk.d("stats2"), pk.d("rdiag2"), pk.d("status"), self.side)
         main.wait_stream(self.side)
@@ -430,7 +437,12 @@ class HostStreamPlan:
     H2D copies of every pair run back to back on one copy stream, and pair
     b's captured compute graph starts on its own stream as soon as pair b's
     copy event fires, so compute overlaps the transfers of the pairs behind
-    it and the step is bounded by the PCIe link, not by copy + compute."""
+    it and the step is bounded by the PCIe link, not by copy + compute.
+    Large pairs (>= BIG_PAIR_BYTES, e.g. the genome-scale cfg2) are enqueued
+    eagerly with one event per matrix instead: the G1 chain runs while G2 is
+    still being copied."""
+
+    BIG_PAIR_BYTES = 1 << 30
 
     def __init__(self, B: int, m: int, p: int, n: int, k1: int, k2: int):
         self.B, self.m, self.p, self.n = B, m, p, n
@@ -438,6 +450,7 @@ class HostStreamPlan:
         self.streams = [torch.cuda.Stream() for _ in range(B)]
         self.copy_stream = torch.cuda.Stream()
         self.events = [torch.cuda.Event() for _ in range(B)]
+        self.events1 = [torch.cuda.Event() for _ in range(B)]
         w = _even(n)
         self.bufs = []
         for _ in range(B):
@@ -465,17 +478,24 @@ class HostStreamPlan:
         self.copy_stream.wait_stream(cur)
         staged = [(self._host(h1, self.m, self.n, "g1"), self._host(h2, self.p, self.n, "g2"))
                   for h1, h2 in host_pairs]
+        big = 8 * (self.m + self.p) * self.n >= self.BIG_PAIR_BYTES
         with torch.cuda.stream(self.copy_stream):
-            for (h1, h2), (d1, d2), ev in zip(staged, self.bufs, self.events):
+            for (h1, h2), (d1, d2), ev1, ev in zip(staged, self.bufs, self.events1, self.events):
                 d1.t.copy_(h1, non_blocking=True)
+                ev1.record(self.copy_stream)
                 d2.t.copy_(h2, non_blocking=True)
                 ev.record(self.copy_stream)
-        for plan, st, ev, (d1, d2), seed in zip(self.plans, self.streams, self.events, self.bufs,
-                                                 seeds):
+        for plan, st, ev1, ev, (d1, d2), seed in zip(self.plans, self.streams, self.events1,
+                                                      self.events, self.bufs, seeds):
             st.wait_stream(cur)
-            st.wait_event(ev)
             with torch.cuda.stream(st):
-                plan.run(d1, d2, seed, q_iters, classify_tol, sync=False)
+                if big:  # per-matrix readiness: chain 1 overlaps the G2 copy
+                    plan.s1.set_seed(seed)
+                    plan.s2.set_seed(int(seed) + 1)
+                    plan.enqueue(d1, d2, q_iters, classify_tol, ready1=ev1, ready2=ev)
+                else:
+                    st.wait_event(ev)
+                    plan.run(d1, d2, seed, q_iters, classify_tol, sync=False)
         for st in self.streams:
             cur.wait_stream(st)
         cur.synchronize()  # the pinned staging (if any) is released only after this
@@ -651,7 +671,11 @@ _SMALL_PLANS: dict = {}
 
 
 def small_batch_plan(B: int, n: int, k: int) -> SmallBatchPlan:
-    key = (B, n, k)
-    if key not in _SMALL_PLANS:
-        _SMALL_PLANS[key] = SmallBatchPlan(B, n, k)
-    return _SMALL_PLANS[key]
+    key = (torch.cuda.current_device(), B, n, k)
+    plan = _SMALL_PLANS.get(key)
+    if plan is None:
+        if len(_SMALL_PLANS) > 4:
+            _SMALL_PLANS.clear()
+        plan = SmallBatchPlan(B, n, k)
+        _SMALL_PLANS[key] = plan
+    return plan
