@@ -608,16 +608,72 @@ def device_matrix(rows, cfg, a_seed, bmat, d, dtype):
     return g
 
 
+def fp64_gemm_roofline(cfg, gmat, rows: int, steps_time_per_pair: float, world: int = 1):
+    """Time the two G-pass DMMA GEMMs (B = Q^T G and Y = G X) live on G's
+    shape (rows x n) with CUDA events on their stream; the slower one is the
+    roofline kernel. Returns (roofline dict, sketch-GEMM TFLOP/s, kernel_us)."""
+    import torch
+
+    from paper_2404_09459_b200 import _native
+    from paper_2404_09459_b200 import device as dv
+
+    L = _native.lib()
+    kp, ldb = dv.ceil16(cfg.k), dv.ceil16(cfg.n)
+    Q = torch.randn(rows, kp, dtype=torch.float64, device="cuda")
+    Q[:, cfg.k:] = 0
+    Bo = torch.zeros(kp, ldb, dtype=torch.float64, device="cuda")
+    Xt = torch.zeros(kp, ldb, dtype=torch.float64, device="cuda")
+    Xt[: cfg.k, : cfg.n] = torch.randn(cfg.k, cfg.n, dtype=torch.float64, device="cuda")
+    Y = torch.zeros(rows, kp, dtype=torch.float64, device="cuda")
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    st = dv.sp(torch.cuda.current_stream())
+
+    def gtq():
+        L.rgsv_gemm_gtq(dv.vp(Q), kp, dv.vp(gmat.t), gmat.ld, dv.vp(Bo), ldb, kp, cfg.n, rows,
+                        dv.vp(scratch), scratch.numel(), st)
+
+    def gx():
+        L.rgsv_gemm_gx(dv.vp(gmat.t), gmat.ld, dv.vp(Xt), ldb, dv.vp(Y), kp, rows, kp, cfg.n,
+                       dv.vp(scratch), scratch.numel(), st)
+
+    t_gtq = time_kernel(gtq)
+    t_gx = time_kernel(gx)
+    flop = 2.0 * rows * cfg.n * cfg.k
+    dom_name, dom_t, dom_k = ("gemm_gtq (B = Q^T G, DMMA)", t_gtq, "k_gtq") if t_gtq >= t_gx \
+        else ("gemm_gx (Y = G X, DMMA)", t_gx, "k_gx")
+    achieved = flop / dom_t / 1e12
+    # sketch-GEMM TFLOP/s over the 2q+2 G passes of both matrices (per rank),
+    # from the per-launch times scaled by each matrix's rows
+    per = cfg.q + 1
+    gemm_time = per * (t_gtq + t_gx) * (cfg.m + cfg.p) / cfg.m
+    sketch = cfg.flops / world / gemm_time / 1e12
+    del Q, Bo, Xt, Y, scratch
+    roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved,
+            "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+            "traffic": committed_traffic(cfg.name, dom_k) if world == 1 else None,
+            "flop_per_launch": flop, "launch_us": dom_t * 1e6,
+            "peak_source": "measured FP64 DMMA issue peak (tools/fp64_peak.cu, "
+                           "profiles/r01_fp64_peak.log; MEASURED_PEAKS.json has no FP64 figure)",
+            "share_of_step": per * 2 * dom_t * (cfg.m + cfg.p) / cfg.m / steps_time_per_pair}
+    return roof, sketch, {"gemm_gtq": t_gtq * 1e6, "gemm_gx": t_gx * 1e6}
+
+
 def run_ours_sharded(args, rank, world):
-    """ONE pair per step, G1/G2 row-sharded over the ranks (genes), every
-    k x k Gram, Z^T and B partial all-reduced with NCCL (dist.py): strong
-    scaling. fp32 configs take the tf32x3 tensor-core chain."""
+    """ONE pair per step, G1/G2 row-sharded over the ranks (genes): each
+    matrix chain is one native rgsv_sketch_project_sharded call per rank with
+    every ||G||^2, k x k Gram, Z^T and B partial all-reduced in-stream by NCCL
+    communicators owned by librgsv (dist.Comm), the two chains on two
+    streams, the small GSVD on rank 0 and broadcast; the whole pair is one
+    CUDA graph per rank after warm-up. Strong scaling. fp32 configs (cfg4)
+    take the tf32x3 tensor-core chain with the same reductions."""
     import torch
     import torch.distributed as dist
 
     from paper_2404_09459_b200 import _native
+    from paper_2404_09459_b200 import device as dv
     from paper_2404_09459_b200 import dist as rdist
-    from paper_2404_09459_b200.workloads import CONFIGS
+    from paper_2404_09459_b200.workloads import CONFIGS, make_pair
 
     cfg = CONFIGS[args.config]
     f32 = cfg.dtype == "f32"
@@ -633,9 +689,11 @@ def run_ours_sharded(args, rank, world):
     s0, s1 = rdist.shard_rows(cfg.p, rank, world)
     g1 = device_matrix(r1 - r0, cfg, 1000 + rank, b1, d, dt)
     g2 = device_matrix(s1 - s0, cfg, 2000 + rank, b2, d, dt)
+    comm = rdist.default_comm()
 
-    def step(i):
-        return rdist.compute_gsv_sharded(g1, g2, cfg.m, cfg.p, cfg.n, cfg.k, cfg.q, seed=i)
+    def step(a, b, i):
+        return rdist.compute_gsv_sharded(a, b, cfg.m, cfg.p, cfg.n, cfg.k, cfg.q, seed=i,
+                                         comm=comm)
 
     def barrier():
         if world > 1:
@@ -643,25 +701,65 @@ def run_ours_sharded(args, rank, world):
         torch.cuda.synchronize()
 
     for i in range(args.warmup):
-        step(i)
+        step(g1, g2, i)
     barrier()
     clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
-    l0 = _native.lib().rgsv_launch_count()
+    l0 = _native.lib().rgsv_launch_count() + dv.GRAPH_REPLAYS[1]
     stream = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.steps):
-        res = step(i)
+        res = step(g1, g2, i)
     e1.record(stream)
     barrier()
-    launches = _native.lib().rgsv_launch_count() - l0
+    launches = _native.lib().rgsv_launch_count() + dv.GRAPH_REPLAYS[1] - l0
     clk = clocks.stop() if clocks else None
     tt = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_max = float(tt.item())
     value = args.steps / t_max
+
+    # e2e: every step copies this rank's shards from pinned host memory
+    h1 = g1.cpu().pin_memory()
+    h2 = g2.cpu().pin_memory()
+    d1 = torch.empty_like(g1)
+    d2 = torch.empty_like(g2)
+
+    def e2e_step(i):
+        d1.copy_(h1, non_blocking=True)
+        d2.copy_(h2, non_blocking=True)
+        return step(d1, d2, i)
+
+    for i in range(min(2, max(args.warmup, 2))):
+        e2e_step(i)
+    barrier()
+    ne = max(3, args.steps // 2)
+    e0.record(stream)
+    for i in range(ne):
+        e2e_step(i)
+    e1.record(stream)
+    barrier()
+    te = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = ne / float(te.item())
+    h2d = (h1.numel() + h2.numel()) * h1.element_size()
+    d2h = int(res.report.plan.pk.nbytes) if hasattr(res.report, "plan") and res.report.plan \
+        else (6 * cfg.n + 8) * 8
+    del d1, d2, h1, h2
+
+    if f32:
+        roof, sketch, kus = None, None, None
+    else:
+        roof, sketch, kus = fp64_gemm_roofline(cfg, dv.to_device(g1, "g1"), r1 - r0,
+                                               t_max / args.steps, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not f32:
+        hg1, hg2 = make_pair(cfg)
+        cpu = cpu_baseline(cfg, args.cpu_sample_seconds, hg1, hg2)
+        del hg1, hg2
     if rank == 0:
         peak = MEASURED_BF16_TFLOPS / 6.0 if f32 else FP64_DMMA_PEAK_TFLOPS
         eff = cfg.flops * value / world / 1e12
@@ -673,15 +771,24 @@ def run_ours_sharded(args, rank, world):
             "dtype": "f32 (3xTF32 tensor cores)" if f32 else "f64",
             "data": "synthetic (device-generated per rank with the workloads.py recipe)",
             "config": {"workload": workload_desc(cfg), "g_bytes": cfg.g_bytes,
-                       "parallelism": f"row-sharded x{world} (NCCL all-reduce of Gram/Z/B)",
+                       "step": "one pair per step, row-sharded over the ranks",
+                       "parallelism": f"row-sharded x{world} ({comm.mode}: all-reduce of "
+                                      "||G||^2 / Gram / Z / B partials, rank-0 small GSVD "
+                                      "broadcast)",
                        "l2": "inputs larger than L2"},
-            "roofline": {"bound": "tensor", "kernel": "whole chain (GEMM flops / step time)",
-                         "achieved": eff, "peak": peak, "unit": "TFLOP/s", "frac": eff / peak,
-                         "traffic": None,
-                         "peak_source": "3xTF32 = measured bf16 / 6" if f32 else
-                                        "measured FP64 DMMA issue peak"},
-            "cpu_baseline": None,
-            "e2e": None,
+            "roofline": roof or {"bound": "tensor", "kernel": "whole chain (GEMM flops / step)",
+                                 "achieved": eff, "peak": peak, "unit": "TFLOP/s",
+                                 "frac": eff / peak, "traffic": None,
+                                 "peak_source": "3xTF32 = measured bf16 / 6"},
+            "sketch_gemm_tflops_per_gpu": sketch,
+            "sketch_gemm_frac_of_peak": sketch / FP64_DMMA_PEAK_TFLOPS if sketch else None,
+            "chain_tflops_per_gpu": eff,
+            "kernel_us": kus,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "path": "dist.compute_gsv_sharded() with each rank's shards copied H2D "
+                            "from pinned host memory every step and the report read back"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "check": {"r": int(res.r), "s": int(res.s)},
@@ -790,40 +897,8 @@ def run_ours(args, rank, world):
     d2h = B * sub.pk.nbytes
 
     # ---- dominant kernel, timed live (CUDA events on its stream)
-    L = _native.lib()
-    kp = dv.ceil16(cfg.k)
-    ldb = dv.ceil16(cfg.n)
-    Q = torch.randn(cfg.m, kp, dtype=torch.float64, device="cuda")
-    Q[:, cfg.k:] = 0
-    Bo = torch.zeros(kp, ldb, dtype=torch.float64, device="cuda")
-    Xt = torch.zeros(kp, ldb, dtype=torch.float64, device="cuda")
-    Xt[: cfg.k, : cfg.n] = torch.randn(cfg.k, cfg.n, dtype=torch.float64, device="cuda")
-    Y = torch.zeros(cfg.m, kp, dtype=torch.float64, device="cuda")
-    scratch = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
-    st = dv.sp(stream)
-    gmat = pair.g1
-
-    def gtq():
-        L.rgsv_gemm_gtq(dv.vp(Q), kp, dv.vp(gmat.t), gmat.ld, dv.vp(Bo), ldb, kp, cfg.n, cfg.m,
-                        dv.vp(scratch), scratch.numel(), st)
-
-    def gx():
-        L.rgsv_gemm_gx(dv.vp(gmat.t), gmat.ld, dv.vp(Xt), ldb, dv.vp(Y), kp, cfg.m, kp, cfg.n,
-                       dv.vp(scratch), scratch.numel(), st)
-
-    t_gtq = time_kernel(gtq)
-    t_gx = time_kernel(gx)
-    flop = 2.0 * cfg.m * cfg.n * cfg.k
-    per_pair = (cfg.q + 1)  # launches of each shape per matrix
-    dom_name, dom_t = ("gemm_gtq (B = Q^T G, DMMA)", t_gtq) if t_gtq >= t_gx else \
-        ("gemm_gx (Y = G X, DMMA)", t_gx)
-    achieved = flop / dom_t / 1e12
-    # sketch-GEMM TFLOP/s over all 2q+2 passes of both matrices, from the
-    # per-launch times scaled by each matrix's rows
-    gemm_time = per_pair * (t_gtq + t_gx) * (cfg.m + cfg.p) / cfg.m
-    sketch_tflops = cfg.flops / gemm_time / 1e12
     step_s = t_max / (args.steps * B)
-    traffic = committed_traffic(cfg.name, "k_gtq" if t_gtq >= t_gx else "k_gx")
+    roof, sketch_tflops, kus = fp64_gemm_roofline(cfg, pair.g1, cfg.m, step_s)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
@@ -845,16 +920,10 @@ def run_ours(args, rank, world):
                        "l2": "inputs larger than L2 (%d x G1+G2 = %.0f MB > 126 MB)"
                              % (B, B * cfg.g_bytes / 1e6),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-            "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved,
-                         "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,
-                         "flop_per_launch": flop, "launch_us": dom_t * 1e6,
-                         "peak_source": "measured FP64 DMMA issue peak (tools/fp64_peak.cu; "
-                                        "MEASURED_PEAKS.json has no FP64 figure)",
-                         "share_of_step": per_pair * 2 * dom_t * (cfg.m + cfg.p) / cfg.m / step_s},
+            "roofline": roof,
             "sketch_gemm_tflops": sketch_tflops,
             "sketch_gemm_frac_of_peak": sketch_tflops / FP64_DMMA_PEAK_TFLOPS,
-            "kernel_us": {"gemm_gtq": t_gtq * 1e6, "gemm_gx": t_gx * 1e6},
+            "kernel_us": kus,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
@@ -868,6 +937,20 @@ def run_ours(args, rank, world):
                       "d2": rep.d2},
         }
         print(json.dumps(line), flush=True)
+
+
+def select_mode(args, world: int) -> str:
+    """Which timed path a run takes: cfg3's many small pairs are independent
+    (replicas at any N); single-pair configs at N > 1 run ONE pair
+    row-sharded over the ranks (strong scaling) unless --replicas."""
+    from paper_2404_09459_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if cfg.batch > 1:
+        return "batch"
+    if args.sharded or (world > 1 and not args.replicas):
+        return "sharded"
+    return "f32" if cfg.dtype == "f32" else "pairs"
 
 
 def main():
@@ -894,14 +977,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2404_09459_b200.workloads import CONFIGS
 
-    if CONFIGS[args.config].batch > 1:
-        run_ours_batch(args, rank, world)
-    elif args.sharded or (world > 1 and not args.replicas):
-        run_ours_sharded(args, rank, world)
-    elif CONFIGS[args.config].dtype == "f32":
-        run_ours_f32(args, rank, world)
-    else:
-        run_ours(args, rank, world)
+    {"batch": run_ours_batch, "sharded": run_ours_sharded, "f32": run_ours_f32,
+     "pairs": run_ours}[select_mode(args, world)](args, rank, world)
     if world > 1:
         import torch.distributed as dist
 

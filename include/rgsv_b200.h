@@ -169,6 +169,40 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
                         double* b_out, int64_t ldb, double* stats, double* rdiag, int* status,
                         void* workspace, size_t workspace_bytes, void* stream);
 
+/* --- (1)-(3) for ONE ROW SHARD of a matrix (multi-GPU) ---
+ * The same chain as rgsv_sketch_project on this rank's contiguous row block
+ * g (m_local x n) of a matrix with m_total rows in all. Every cross-rank sum
+ * goes through `allreduce` (in-stream, on `stream`): ||G||_F^2 (1 value),
+ * each tall CholeskyQR pass's k x k Gram (kp*kp values), every power step's
+ * Z^T = Q^T G (kp*ldb values) and the projection B (kp*ldb values). The
+ * shifted CholeskyQR uses m_total; the wide QR of Z runs redundantly on
+ * every rank; Q stays row-sharded (q_out: m_local x kp); B, stats and rdiag
+ * come out replicated. Pass rgsv_nccl_allreduce with an NCCL communicator
+ * as ctx (below), or any function with this signature (a gloo/MPI wrapper);
+ * allreduce == NULL requires m_local == m_total (single rank).
+ * Replaces, per rank, the Y = G Omega / Q^H G products of
+ * rangefinder.py:115,123 and engine.py:255-256. */
+typedef int (*rgsv_allreduce_fn)(double* buf, int64_t count, void* stream, void* ctx);
+int rgsv_sketch_project_sharded(const double* g, int64_t ldg, int64_t m_local, int64_t m_total,
+                                int64_t n, const double* omega_t, int64_t ld_omega, int k, int q,
+                                double* q_out, double* b_out, int64_t ldb, double* stats,
+                                double* rdiag, int* status, rgsv_allreduce_fn allreduce,
+                                void* allreduce_ctx, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
+/* NCCL (over NVLink / NVSwitch) for the sharded chain, resolved at run time
+ * from the libnccl.so.2 the host process loaded (no link-time dependency).
+ * rgsv_nccl_version: NCCL_VERSION code, -1 when NCCL is not loadable.
+ * get_unique_id fills 128 bytes on one rank; every rank passes them to
+ * comm_init. rgsv_nccl_allreduce has the rgsv_allreduce_fn signature, ctx = comm:
+ * in-place fp64 sum. rgsv_nccl_broadcast: `bytes` bytes from `root`. */
+int rgsv_nccl_version(void);
+int rgsv_nccl_get_unique_id(void* id_out);
+int rgsv_nccl_comm_init(void** comm_out, int nranks, const void* id, int rank);
+int rgsv_nccl_comm_destroy(void* comm);
+int rgsv_nccl_allreduce(double* buf, int64_t count, void* stream, void* comm);
+int rgsv_nccl_broadcast(void* buf, int64_t bytes, int root, void* stream, void* comm);
+
 /* --- (4) small GSVD -------------------------------------------------------
  * Replaces engine.py:257-261 (reduced_qr of vstack(c1, c2), L blocks) and
  * engine._singular_values (engine.py:228-231) for the two L blocks:

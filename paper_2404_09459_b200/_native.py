@@ -62,6 +62,14 @@ SIGNATURES = {
     "rgsv_sketch_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "rgsv_sketch_project": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _i32, _i32, _p, _p, _i64, _p,
                                    _p, _p, _p, _sz, _p]),
+    "rgsv_sketch_project_sharded": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _i64, _i32, _i32, _p,
+                                           _p, _i64, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "rgsv_nccl_version": (_i32, []),
+    "rgsv_nccl_get_unique_id": (_i32, [_p]),
+    "rgsv_nccl_comm_init": (_i32, [_p, _i32, _p, _i32]),
+    "rgsv_nccl_comm_destroy": (_i32, [_p]),
+    "rgsv_nccl_allreduce": (_i32, [_p, _i64, _p, _p]),
+    "rgsv_nccl_broadcast": (_i32, [_p, _i64, _i32, _p, _p]),
     "rgsv_small_gsvd_workspace_bytes": (_sz, [_i32, _i32, _i64]),
     "rgsv_small_gsvd": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _i64, _p, _p, _p, _p, _p, _sz,
                                _p]),

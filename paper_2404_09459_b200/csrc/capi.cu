@@ -321,9 +321,25 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
                         const double* omega_t, int64_t ld_omega, int k, int q, double* q_out,
                         double* b_out, int64_t ldb, double* stats, double* rdiag, int* status,
                         void* workspace, size_t workspace_bytes, void* stream) {
+  return rgsv_sketch_project_sharded(g, ldg, m, m, n, omega_t, ld_omega, k, q, q_out, b_out, ldb,
+                                     stats, rdiag, status, nullptr, nullptr, workspace,
+                                     workspace_bytes, stream);
+}
+
+int rgsv_sketch_project_sharded(const double* g, int64_t ldg, int64_t m, int64_t m_total,
+                                int64_t n, const double* omega_t, int64_t ld_omega, int k, int q,
+                                double* q_out, double* b_out, int64_t ldb, double* stats,
+                                double* rdiag, int* status, rgsv_allreduce_fn allreduce,
+                                void* allreduce_ctx, void* workspace, size_t workspace_bytes,
+                                void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (m < 1 || n < 1 || k < 1 || q < 0) return RGSV_ERR_DIMENSION;
-  if (k > m || k > n) return RGSV_ERR_VALIDATION;  // rangefinder.py:88-91
+  if (m < 1 || n < 1 || k < 1 || q < 0 || m_total < m) return RGSV_ERR_DIMENSION;
+  if (!allreduce && m_total != m) return RGSV_ERR_VALIDATION;
+  if (k > m_total || k > n) return RGSV_ERR_VALIDATION;  // rangefinder.py:88-91
+  Reducer red;
+  red.fn = allreduce;
+  red.ctx = allreduce_ctx;
+  const Reducer* rp = allreduce ? &red : nullptr;
   const int64_t kp = ceil16(k), ldn = ceil16(n);
   if (kp > 512) return RGSV_ERR_DIMENSION;
   if (ldg < n || ld_omega < n || ldb < n || (ldg & 1) || (ld_omega & 1) || (ldb & 1))
@@ -362,6 +378,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
   if (int e = gemm_gx(s, st)) return e;
   if (ss_units > 4096) return RGSV_ERR_WORKSPACE;
   if (int e = launch_sum(ss, ss_units, stats, st)) return e;
+  if (int e = red(stats, 1, st)) return e;  // ||G||_F^2 over all row blocks
   // (2) Q = qr(Y).q  (rangefinder.py:119)
   double* qres = nullptr;
   // Every orthonormalisation is full shifted CholeskyQR3. (Fewer passes for
@@ -370,7 +387,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
   // the last Y beyond what CholeskyQR3 resolves (full-span angle 8e-5,
   // breakdowns) and two passes still miss the stage tolerances.)
   if (int e = cholqr3_tall(y, q_out, m, k, (int)kp, gram, linv, rd_ws, scratch, sb, status, &qres,
-                           st, q == 0 ? 3 : kIntermediatePasses))
+                           st, q == 0 ? 3 : kIntermediatePasses, rp, m_total))
     return e;
   for (int it = 0; it < q; ++it) {
     // Z^T = Q^T G, Qhat = qr(Z).q, Y = G Qhat, Q = qr(Y).q
@@ -388,6 +405,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
     p.scratch_bytes = sb;
     p.max_split = proj_split();
     if (int e = gemm_gtq(p, st)) return e;
+    if (int e = red(z, kp * ldn, st)) return e;  // Z^T partials of the row blocks
     double* qt = nullptr;
     if (int e = cholqr3_wide(z, z2, n, ldn, k, (int)kp, gram, linv, rinv, rd_ws, scratch, sb,
                              status, &qt, st, kIntermediatePasses))
@@ -399,7 +417,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
     y2.ss_units = nullptr;
     if (int e = gemm_gx(y2, st)) return e;
     if (int e = cholqr3_tall(y, q_out, m, k, (int)kp, gram, linv, rd_ws, scratch, sb, status,
-                             &qres, st, it == q - 1 ? 3 : kIntermediatePasses))
+                             &qres, st, it == q - 1 ? 3 : kIntermediatePasses, rp, m_total))
       return e;
   }
   // (3) B = Q^T G (engine.py:255) and its energy (rangefinder.py:123)
@@ -417,6 +435,7 @@ int rgsv_sketch_project(const double* g, int64_t ldg, int64_t m, int64_t n,
   p.scratch_bytes = sb;
   p.max_split = proj_split();
   if (int e = gemm_gtq(p, st)) return e;
+  if (int e = red(b_out, kp * ldb, st)) return e;  // B partials -> replicated B
   if (int e = launch_sumsq(b_out, ldb, kp, n, stats + 1, ss, 1024, st)) return e;
   if (rdiag) {
     if (cudaMemcpyAsync(rdiag, rd_ws, k * sizeof(double), cudaMemcpyDeviceToDevice, st) !=

@@ -77,9 +77,22 @@ struct Workspace {
 // `passes` = 3 gives shifted CholeskyQR3 (orthonormal Q); 1 gives one shifted
 // pass, Y R1^{-1}: a triangular transform of Y, enough for intermediate bases
 // whose span (and nested leading spans) is all that is used downstream.
+// Row-sharded use: `red` all-reduces each pass's Gram partial over the
+// ranks (Y is this rank's row block) and `shift_rows` is the global row
+// count of the shift (defaults to m).
+struct Reducer {
+  rgsv_allreduce_fn fn = nullptr;
+  void* ctx = nullptr;
+  int operator()(double* buf, int64_t count, cudaStream_t st) const {
+    if (!fn || count <= 0) return 0;
+    return fn(buf, count, reinterpret_cast<void*>(st), ctx) == 0 ? 0 : RGSV_ERR_CUDA;
+  }
+};
+
 int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram, double* linv,
                  double* rdiag, double* scratch, size_t scratch_bytes, int* status,
-                 double** q_out, cudaStream_t st, int passes = 3);
+                 double** q_out, cudaStream_t st, int passes = 3, const Reducer* red = nullptr,
+                 int64_t shift_rows = -1);
 
 // Shifted CholeskyQR3 of Z = B^T where B is kp x n row-major (ld ldn):
 // returns Qhat^T (kp x n) in *qt_out (one of b / tmp).

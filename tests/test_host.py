@@ -209,8 +209,8 @@ def test_bench_reference_arm_contract():
 
 
 def test_sharded_bench_mode_is_wired():
-    """bench.py --sharded routes cfg2/cfg4 to the row-sharded strong-scaling
-    driver (dist.compute_gsv_sharded); the fp32 shards take the tf32 chain."""
+    """bench.py's default is cfg2; N > 1 routes single-pair configs to the
+    row-sharded strong-scaling driver (dist.compute_gsv_sharded)."""
     import os
     import sys
 
@@ -222,7 +222,17 @@ def test_sharded_bench_mode_is_wired():
     sys.argv = ["bench.py", "--sharded", "--config", "cfg4"]
     args = bench.parse()
     assert args.sharded and args.config == "cfg4"
-    assert callable(bench.run_ours_sharded) and callable(rdist.sharded_chain_f32)
+    assert bench.select_mode(args, 1) == "sharded"
+    sys.argv = ["bench.py"]
+    args = bench.parse()
+    assert args.config == "cfg2"  # the metric's config by default
+    assert bench.select_mode(args, 1) == "pairs"
+    assert bench.select_mode(args, 8) == "sharded"  # strong scaling at N > 1
+    sys.argv = ["bench.py", "--replicas"]
+    assert bench.select_mode(bench.parse(), 8) == "pairs"
+    sys.argv = ["bench.py", "--config", "cfg3"]
+    assert bench.select_mode(bench.parse(), 8) == "batch"
+    assert callable(bench.run_ours_sharded) and callable(rdist.compute_gsv_sharded)
     # balanced contiguous gene blocks of the genome-scale configs
     for cfg in ("cfg2", "cfg4"):
         m = CONFIGS[cfg].m
