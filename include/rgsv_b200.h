@@ -214,6 +214,18 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
                     int64_t n, double* sv1, double* sv2, int* nsv, int* status, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* Householder QR (LAPACK dgeqrf + dorgqr semantics) of the M x N matrix
+ * stacked from [a1 (m1 rows); a2 (m2 rows)] (a2 may be NULL with m2 = 0),
+ * M = m1 + m2 <= 1408: q (M x K) and r (K x N, upper trapezoid; may be
+ * NULL), K = min(M, N), with the phase fix diag(R) >= 0 when phase_fix != 0.
+ * Replaces core.reduced_qr (core.py:79-96: numpy.linalg.qr + sign fix),
+ * tall AND wide, and the stacked QR of engine.py:257. Many CTAs, one
+ * cooperative launch. */
+size_t rgsv_dense_qr_workspace_bytes(int M, int N);
+int rgsv_dense_qr(const double* a1, int64_t lda1, int m1, const double* a2, int64_t lda2,
+                  int m2, int N, double* q, int64_t ldq, double* r, int64_t ldr, int phase_fix,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
 /* --- (5) spectrum + comparative quantities -------------------------------
  * Replaces engine.spectrum_from_l_blocks (engine.py:189-225, merged
  * completion), classify_spectrum (engine.py:164-186) and analysis.py:37-79
@@ -291,6 +303,11 @@ int rgsv_gemm_gtq(const double* a, int64_t lda, const double* b, int64_t ldb, do
 int rgsv_chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv,
                   double* rinv, double* rdiag, int* status, void* stream);
 /* Debug: one small Householder QR launch recording clock64() phase stamps. */
+/* Debug: rgsv_dense_qr of one M x N matrix with globaltimer stamps (ns) of
+ * CTA 0 at each phase boundary in prof[0..254]; prof[255] = stamp count. */
+int rgsv_debug_dense_qr_profile(const double* a, int64_t lda, int M, int N, double* q,
+                                void* workspace, size_t workspace_bytes, long long* prof,
+                                void* stream);
 int rgsv_debug_householder_profile(const double* b1, int64_t ld1, int l1, const double* b2,
                                    int64_t ld2, int l2, double* q, int64_t ldq, long long* prof,
                                    void* stream);

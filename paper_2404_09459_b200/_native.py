@@ -73,6 +73,9 @@ SIGNATURES = {
     "rgsv_small_gsvd_workspace_bytes": (_sz, [_i32, _i32, _i64]),
     "rgsv_small_gsvd": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _i64, _p, _p, _p, _p, _p, _sz,
                                _p]),
+    "rgsv_dense_qr_workspace_bytes": (_sz, [_i32, _i32]),
+    "rgsv_dense_qr": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _i32, _p, _i64, _p, _i64, _i32, _p,
+                             _sz, _p]),
     "rgsv_comparative": (_i32, [_p, _p, _p, _i64, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "rgsv_spectrum_quantities": (_i32, [_p, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "rgsv_entropy": (_i32, [_p, _i64, _p, _p]),
@@ -82,6 +85,7 @@ SIGNATURES = {
     "rgsv_gemm_gtq": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "rgsv_chol_inv": (_i32, [_p, _i32, _i32, _i64, _p, _p, _p, _p, _p]),
     "rgsv_debug_householder_profile": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _p, _i64, _p, _p]),
+    "rgsv_debug_dense_qr_profile": (_i32, [_p, _i64, _i32, _i32, _p, _p, _sz, _p, _p]),
     "rgsv_debug_chol_profile": (_i32, [_p, _i32, _i32, _p, _p, _p, _p]),
     "rgsv_sumsq": (_i32, [_p, _i64, _i64, _i64, _p, _p, _sz, _p]),
     "rgsv_f32_split": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _i32, _p, _p, _sz, _p]),

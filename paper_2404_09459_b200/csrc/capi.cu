@@ -1,4 +1,5 @@
 // extern "C" boundary (include/rgsv_b200.h) and the native pipeline driver.
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -448,7 +449,8 @@ int rgsv_sketch_project_sharded(const double* g, int64_t ldg, int64_t m, int64_t
 // ---------------------------------------------------------------- small GSVD
 namespace {
 struct SmallLayout {
-  size_t s, s2, t, t2, gram, linv, rinv, rdiag, v1, v2, scratch, total, scratch_bytes;
+  size_t s, s2, t, t2, gram, linv, rinv, rdiag, v1, v2, scratch, hh, sync, total, scratch_bytes,
+      hh_bytes;
   int64_t lp, lds, kpn;
 };
 SmallLayout small_layout(int l1, int l2, int64_t n) {
@@ -480,10 +482,41 @@ SmallLayout small_layout(int l1, int l2, int64_t n) {
   L.v2 = take((size_t)(l2 + 1) * (rmax + 1) * 8);
   L.scratch_bytes = split_scratch_bytes(l, n, kmax) + (size_t)kSMs * kmax * kmax * 8;
   L.scratch = take(L.scratch_bytes);
+  // multi-CTA Householder of the leading l x l block (wide) or of S (tall)
+  L.hh_bytes = (l <= kHhMaxRows) ? hhqr_workspace_bytes((int)l, (int)(l <= n ? l : n)) : 0;
+  L.hh = take(L.hh_bytes);
+  L.sync = take(bjacobi_sync_bytes());
   L.total = off;
   return L;
 }
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+// Stacked sizes l served by the multi-CTA Householder (k_hhqr) rather than
+// the one-CTA register kernel, and vector counts served by the blocked
+// Jacobi (k_bjacobi) rather than the one-CTA Jacobi (measured crossovers,
+// DESIGN.md §4b; RGSV_HH_MIN / RGSV_BJ_MIN override them).
+int hh_min_l() {
+  static const int v = env_int("RGSV_HH_MIN", 129);
+  return v;
+}
+int bj_min_nv() {
+  static const int v = env_int("RGSV_BJ_MIN", 33);
+  return v;
+}
 }  // namespace
+
+// Row-vector Jacobi dispatch: the blocked multi-CTA kernel for larger jobs.
+static int jacobi_dispatch(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1,
+                           double* v2, int64_t ld2, int nv2, int len2, double* sv2, int* nsv2,
+                           int* status, void* sync, cudaStream_t st) {
+  const int nv = nv1 > nv2 ? nv1 : nv2;
+  if (sync && (nv >= bj_min_nv() || nv > 2048))
+    return bjacobi(v1, ld1, nv1, len1, sv1, nsv1, v2, ld2, nv2, len2, sv2, nsv2, status, sync, st);
+  return launch_jacobi(v1, ld1, nv1, len1, sv1, nsv1, v2, ld2, nv2, len2, sv2, nsv2, status, st);
+}
 
 size_t rgsv_small_gsvd_workspace_bytes(int l1, int l2, int64_t n) {
   return small_layout(l1, l2, n).total;
@@ -511,12 +544,30 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
   double* v2 = reinterpret_cast<double*>(ws + L.v2);
   double* scratch = reinterpret_cast<double*>(ws + L.scratch);
   const size_t sb = L.scratch_bytes;
+  void* sync = ws + L.sync;
   const int64_t lp = L.lp, lds = L.lds;
 
   double* Q = nullptr;
   int64_t ldq = 0;
   int r = 0;
-  if (l <= n && l <= 512) {
+  if (l <= n && l >= hh_min_l() && l <= kHhMaxRows) {
+    // wide S: Q of the leading l x l block (= Q of S), blocked Householder
+    // over many CTAs (dgeqrf + dorgqr, one cooperative launch)
+    Q = T;
+    ldq = lp;
+    if (int e = hhqr(b1, ldb1, l1, b2, ldb2, l2, l, Q, ldq, nullptr, 0, 0, ws + L.hh, L.hh_bytes,
+                     st))
+      return e;
+    r = l;
+  } else if (l > n && l <= kHhMaxRows) {
+    // tall stacked matrix (l > n): thin Q (l x n) of the Householder QR
+    Q = S;
+    ldq = lds;
+    if (int e = hhqr(b1, ldb1, l1, b2, ldb2, l2, (int)n, Q, ldq, nullptr, 0, 0, ws + L.hh,
+                     L.hh_bytes, st))
+      return e;
+    r = (int)n;
+  } else if (l <= n && l <= 512) {
     // wide S: Householder Q of the leading l x l block (= Q of S, see
     // k_householder_small), one CTA (shared memory, or L2-resident scratch)
     Q = T;
@@ -582,7 +633,32 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
     nv2 = r; len2 = l2; ld2 = l2;
     if (int e = launch_copy_block(v2, ld2, Q + (int64_t)l1 * ldq, ldq, r, l2, 1, st)) return e;
   }
-  return launch_jacobi(v1, ld1, nv1, len1, sv1, nsv, v2, ld2, nv2, len2, sv2, nsv + 1, status, st);
+  return jacobi_dispatch(v1, ld1, nv1, len1, sv1, nsv, v2, ld2, nv2, len2, sv2, nsv + 1, status,
+                         sync, st);
+}
+
+size_t rgsv_dense_qr_workspace_bytes(int M, int N) {
+  if (M < 1 || N < 1 || M > kHhMaxRows) return 0;
+  return hhqr_workspace_bytes(M, N);
+}
+
+int rgsv_dense_qr(const double* a1, int64_t lda1, int m1, const double* a2, int64_t lda2,
+                  int m2, int N, double* q, int64_t ldq, double* r, int64_t ldr, int phase_fix,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+  if (m1 < 0 || m2 < 0 || N < 1 || m1 + m2 < 1 || m1 + m2 > kHhMaxRows) return RGSV_ERR_DIMENSION;
+  if ((m2 > 0 && !a2) || !a1 || !q) return RGSV_ERR_VALIDATION;
+  const int K = (m1 + m2) < N ? (m1 + m2) : N;
+  if (ldq < K || (r && ldr < N)) return RGSV_ERR_DIMENSION;
+  return hhqr(a1, lda1, m1, a2, lda2, m2, N, q, ldq, r, ldr, phase_fix, workspace,
+              workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rgsv_debug_dense_qr_profile(const double* a, int64_t lda, int M, int N, double* q,
+                                void* workspace, size_t workspace_bytes, long long* prof,
+                                void* stream) {
+  if (M < 1 || N < 1 || M > kHhMaxRows) return RGSV_ERR_DIMENSION;
+  return hhqr(a, lda, M, nullptr, 0, 0, N, q, M < N ? M : N, nullptr, 0, 0, workspace,
+              workspace_bytes, reinterpret_cast<cudaStream_t>(stream), prof);
 }
 
 int rgsv_comparative(const double* sv1, const int* nsv, const double* sv2, int64_t n,
@@ -612,7 +688,7 @@ int rgsv_entropy(const double* p, int64_t n, double* scalars, void* stream) {
 }
 
 size_t rgsv_svd_values_workspace_bytes(int rows, int cols) {
-  return (size_t)rows * cols * sizeof(double) + 256;
+  return al256((size_t)rows * cols * sizeof(double)) + bjacobi_sync_bytes();
 }
 
 int rgsv_svd_values(const double* a, int64_t lda, int rows, int cols, double* sv, int* nsv,
@@ -631,7 +707,8 @@ int rgsv_svd_values(const double* a, int64_t lda, int rows, int cols, double* sv
     len = rows;
     if (int e = launch_copy_block(v, len, a, lda, cols, rows, 1, st)) return e;
   }
-  return launch_jacobi(v, len, nv, len, sv, nsv, v, len, 0, len, sv, nsv + 1, status, st);
+  void* sync = static_cast<char*>(workspace) + al256((size_t)rows * cols * sizeof(double));
+  return jacobi_dispatch(v, len, nv, len, sv, nsv, v, len, 0, len, sv, nsv + 1, status, sync, st);
 }
 
 int rgsv_gemm_gx(const double* a, int64_t lda, const double* bt, int64_t ldb, double* c,

@@ -100,4 +100,19 @@ int cholqr3_wide(double* b, double* tmp, int64_t n, int64_t ldn, int k, int kp, 
                  double* linv, double* rinv, double* rdiag, double* scratch, size_t scratch_bytes,
                  int* status, double** qt_out, cudaStream_t st, int passes = 3);
 
+// Multi-CTA dense factorizations (dense.cu), one cooperative launch each.
+// Householder QR of [b1 (m1 rows); b2 (m2 rows)] (M x N, M <= 1408): Q (M x
+// K) and optionally R (K x N), K = min(M, N); phase_fix makes diag(R) >= 0.
+constexpr int kHhMaxRows = 1408;
+size_t hhqr_workspace_bytes(int M, int N);
+int hhqr(const double* b1, int64_t ld1, int m1, const double* b2, int64_t ld2, int m2, int N,
+         double* q, int64_t ldq, double* r, int64_t ldr, int phase_fix, void* ws, size_t ws_bytes,
+         cudaStream_t st, long long* prof = nullptr);
+// Singular values of the rows of two matrices by blocked one-sided Jacobi
+// (either job may be empty); `sync` holds bjacobi_sync_bytes() of scratch.
+size_t bjacobi_sync_bytes();
+int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, double* v2,
+            int64_t ld2, int nv2, int len2, double* sv2, int* nsv2, int* status, void* sync,
+            cudaStream_t st);
+
 }  // namespace rgsv
