@@ -4,7 +4,8 @@
 ``numpy.random.default_rng``, core.py:60-76) because the sketches must use
 the reference's own Ω; everything that touches the matrices themselves
 runs on the B200 (``frobenius_norm``/``sum_sq`` through the device
-sum-of-squares kernel, ``reduced_qr`` through shifted CholeskyQR3).
+sum-of-squares kernel, ``reduced_qr`` through the multi-CTA Householder
+kernel or shifted CholeskyQR3). No cuBLAS/cuSOLVER call is made.
 """
 
 from __future__ import annotations
@@ -75,56 +76,143 @@ def frobenius_norm(m) -> float:
     return math.sqrt(sum_sq(as_matrix(m)))
 
 
+HH_MAX_ROWS = 1408  # rgsv_dense_qr (multi-CTA Householder) row limit
+CHOL_MAX_COLS = 4096  # blocked-Cholesky limit of the CholeskyQR3 route
+
+
 def reduced_qr(m) -> QrFactors:
-    """Reduced QR of a tall full-column-rank matrix (cols <= 1024) by shifted
-    CholeskyQR3 on the B200; R has a positive diagonal, which is the
-    reference's phase convention (core.py:79-96)."""
+    """Reduced QR with the reference's phase convention diag(R) >= 0
+    (core.py:79-96), tall or wide, on the B200:
+
+    * rows <= 1408: blocked Householder over many CTAs (rgsv_dense_qr), the
+      LAPACK dgeqrf/dorgqr algorithm numpy.linalg.qr runs; rank deficiency
+      is permitted exactly as in the reference (R_jj ~ 0);
+    * taller matrices (cols <= 4096): shifted CholeskyQR3, R = Q^T A; a
+      CholeskyQR breakdown (numerical rank deficiency) falls back to the
+      one-CTA Householder kernel (cols <= 1024);
+    * wide matrices with more than 1408 rows: CholeskyQR3 of the leading
+      rows x rows block (rows <= 4096), R = Q^T A.
+    """
     g = as_matrix(m)
     rows, cols = g.rows, g.cols
-    if rows < cols:
-        raise DimensionError("B200 reduced_qr supports tall matrices (rows >= cols)")
+    if rows <= HH_MAX_ROWS:
+        q, r = dense_qr(g.t, rows, None, 0, cols)
+        return QrFactors(q.cpu().numpy(), r.cpu().numpy())
+    if rows >= cols:
+        if _dev.ceil16(cols) > CHOL_MAX_COLS:
+            raise DimensionError(f"B200 reduced_qr supports at most {CHOL_MAX_COLS} columns")
+        q, r = tall_qr(g.t, rows, cols)
+        return QrFactors(q.cpu().numpy(), r.cpu().numpy())
+    if _dev.ceil16(rows) > CHOL_MAX_COLS:
+        raise DimensionError(f"B200 reduced_qr of a wide matrix supports at most "
+                             f"{CHOL_MAX_COLS} rows")
+    q, _ = tall_qr(g.t[:, :rows], rows, rows)
+    r = _gemm_at_b(q, g.t, rows, cols, rows)
+    return QrFactors(q.cpu().numpy(), torch.triu(r).cpu().numpy())
+
+
+def dense_qr(a1: torch.Tensor, m1: int, a2, m2: int, n: int, want_r: bool = True,
+             phase_fix: bool = True):
+    """Householder QR of the row stack [a1 (m1 rows); a2 (m2 rows)] (device
+    tensors, fp64, m1 + m2 <= 1408): Q (M x K) and R (K x n) tensors,
+    K = min(M, n) -- rgsv_dense_qr, one cooperative launch."""
+    L = lib()
+    M = m1 + m2
+    K = min(M, n)
+    q = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    r = torch.empty((K, n), dtype=torch.float64, device="cuda") if want_r else None
+    nb = int(L.rgsv_dense_qr_workspace_bytes(M, n))
+    if nb == 0:
+        raise DimensionError(f"Householder QR supports at most {HH_MAX_ROWS} rows, got {M}")
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    st = _dev.sp(torch.cuda.current_stream())
+    check(L.rgsv_dense_qr(_dev.vp(a1), a1.stride(0), m1, _dev.vp(a2) if a2 is not None else None,
+                          a2.stride(0) if a2 is not None else 0, m2, n, _dev.vp(q), K,
+                          _dev.vp(r) if r is not None else None, n if r is not None else 0,
+                          1 if phase_fix else 0, _dev.vp(ws), nb, st), "rgsv_dense_qr")
+    return q, r
+
+
+def _scratch_for(kp: int) -> torch.Tensor:
+    """Split-K partial storage for the GEMMs of a kp-wide CholeskyQR: tail
+    tiles of the G X passes (<= 148 x 128 rows) or a few kp x kp Gram
+    partials, whichever is larger."""
+    return torch.empty(max(148 * 128 * max(kp, 128), 4 * kp * kp) + 4096, dtype=torch.float64,
+                       device="cuda")
+
+
+def _gemm_at_b(a: torch.Tensor, b: torch.Tensor, m_out: int, n_out: int, rows: int):
+    """C (m_out x n_out) = A^T B over `rows` rows (rgsv_gemm_gtq, DMMA)."""
+    L = lib()
+    c = torch.empty((m_out, n_out + (n_out & 1)), dtype=torch.float64, device="cuda")
+    scratch = _scratch_for(_dev.ceil16(max(m_out, 16)))
+    check(L.rgsv_gemm_gtq(_dev.vp(a), a.stride(0), _dev.vp(b), b.stride(0), _dev.vp(c),
+                          c.stride(0), m_out, n_out, rows, _dev.vp(scratch),
+                          scratch.numel() * 8, _dev.sp(torch.cuda.current_stream())), "gtq")
+    return c[:, :n_out]
+
+
+def tall_qr(a: torch.Tensor, rows: int, cols: int):
+    """Reduced QR of a tall device matrix (rows x cols view, fp64): shifted
+    CholeskyQR3 (R = Q^T A, diag > 0), or -- when CholeskyQR breaks down on
+    a numerically rank-deficient matrix -- the one-CTA Householder kernel
+    with the reference's phase fix. Returns (Q rows x cols, R cols x cols)."""
     kp = _dev.ceil16(cols)
-    if kp > 1024:
-        raise DimensionError("B200 reduced_qr supports at most 1024 columns")
     y = torch.zeros((rows, kp), dtype=torch.float64, device="cuda")
-    y[:, :cols].copy_(g.t[:, :cols])
-    r = _qr_in_place(y, rows, cols)
-    return QrFactors(y[:, :cols].cpu().numpy(), r[:cols, :cols].cpu().numpy())
+    y[:, :cols].copy_(a[:, :cols])
+    try:
+        _qr_in_place(y, rows, cols)
+        q = y[:, :cols]
+        r = torch.triu(_gemm_at_b(q, a, cols, cols, rows))
+        d = torch.diagonal(r).abs()
+        # shifted CholeskyQR3 is accurate up to cond ~ 1/u; a (near) rank
+        # deficient matrix (the shift keeps the Cholesky alive) goes to the
+        # Householder kernel, which reproduces LAPACK's R_jj ~ 0
+        if kp > 1024 or float(d.min()) > 1e-10 * float(d.max()):
+            return q, r
+        raise RankDeficiencyError("near rank deficient")
+    except RankDeficiencyError:
+        if kp > 1024:
+            raise
+        L = lib()
+        w = y.clone()
+        w[:, :cols].copy_(a[:, :cols])
+        w[:, cols:] = 0.0
+        qq = torch.zeros((rows, kp), dtype=torch.float64, device="cuda")
+        rd = torch.zeros(kp, dtype=torch.float64, device="cuda")
+        tau = torch.zeros(kp, dtype=torch.float64, device="cuda")
+        check(L.rgsv_householder_qr(_dev.vp(w), kp, rows, cols, _dev.vp(qq), kp, _dev.vp(rd),
+                                    _dev.vp(tau), _dev.sp(torch.cuda.current_stream())),
+              "householder_qr")
+        q = qq[:, :cols]
+    r = _gemm_at_b(q, a, cols, cols, rows)
+    return q, torch.triu(r)
 
 
-def _qr_in_place(y: torch.Tensor, rows: int, k: int) -> torch.Tensor:
-    """CholQR3 on the device through the C-ABI building blocks; y (rows x kp)
-    is replaced by Q, returns R (kp x kp) = R3 R2 R1."""
+def _qr_in_place(y: torch.Tensor, rows: int, k: int) -> None:
+    """Shifted CholeskyQR3 on the device through the C-ABI building blocks;
+    y (rows x kp) is replaced by Q. RankDeficiencyError on breakdown."""
     L = lib()
     kp = y.shape[1]
     st = _dev.sp(torch.cuda.current_stream())
     gram = torch.empty((kp, kp), dtype=torch.float64, device="cuda")
     linv = torch.empty(kp * kp + kp * (kp + 1), dtype=torch.float64, device="cuda")
-    rinv = torch.empty((kp, kp), dtype=torch.float64, device="cuda")
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
-    scratch = torch.empty(148 * kp * max(kp, 128) + 4096, dtype=torch.float64, device="cuda")
+    scratch = _scratch_for(kp)
     tmp = torch.empty_like(y)
-    r_acc = torch.eye(kp, dtype=torch.float64, device="cuda")
     src, dst = y, tmp
     for step in range(3):
         check(L.rgsv_gemm_gtq(_dev.vp(src), kp, _dev.vp(src), kp, _dev.vp(gram), kp, kp, kp, rows,
                               _dev.vp(scratch), scratch.numel() * 8, st), "gram")
         check(L.rgsv_chol_inv(_dev.vp(gram), k, kp, rows if step == 0 else 0, _dev.vp(linv),
-                              _dev.vp(rinv), None, _dev.vp(status), st), "chol")
+                              None, None, _dev.vp(status), st), "chol")
         check(L.rgsv_gemm_gx(_dev.vp(src), kp, _dev.vp(linv), kp, _dev.vp(dst), kp, rows, kp, kp,
                              _dev.vp(scratch), scratch.numel() * 8, st), "trsm")
-        # R_step = (Rinv)^-1 accumulated on the device: R_acc <- R_step R_acc
-        rstep = torch.linalg.solve_triangular(rinv, torch.eye(kp, dtype=torch.float64,
-                                                              device="cuda"), upper=True)
-        r_acc = rstep @ r_acc
         src, dst = dst, src
     if int(status.item()) != 0:
-        from .errors import RankDeficiencyError
-
         raise RankDeficiencyError("CholeskyQR breakdown: matrix is numerically rank deficient")
     if src is not y:
         y.copy_(src)
-    return r_acc
 
 
 __all__ = ["REAL", "COMPLEX", "QrFactors", "SvdFactors", "as_matrix", "gaussian_matrix",
@@ -172,12 +260,13 @@ def pseudoinverse_norm(m) -> float:
     except ConvergenceError:
         # exactly dependent columns can stall the values-only Jacobi; the
         # CholeskyQR route then reports the rank deficiency like the reference
-        if _dev.ceil16(cols) > 1024:
+        if _dev.ceil16(cols) > CHOL_MAX_COLS:
             raise
         y = torch.zeros((rows, _dev.ceil16(cols)), dtype=torch.float64, device="cuda")
         y[:, :cols] = g.t
-        r = _qr_in_place(y, rows, cols)[:cols, :cols].contiguous()  # raises RankDeficiencyError
-        sv = _jacobi_values(r, cols, cols)
+        _qr_in_place(y, rows, cols)  # raises RankDeficiencyError
+        r = _gemm_at_b(y[:, :cols], g.t, cols, cols, rows)
+        sv = _jacobi_values(torch.triu(r).contiguous(), cols, cols)
     smax, smin = float(sv[0]), float(sv[-1])
     if smin <= 1e-13 * smax:
         raise RankDeficiencyError(f"smallest singular value {smin:.3e} below rank threshold "

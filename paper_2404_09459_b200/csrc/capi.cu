@@ -578,7 +578,7 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
     // S = [B1; B2] (l x n, wide). S^T = P T (CholQR3 on S^T), so
     // range(S) = range(T^T) and the Q of qr(S) is the Q of qr(T^T).
     if (int e = launch_stack(S, lds, b1, ldb1, l1, b2, ldb2, l2, (int)lp, n, st)) return e;
-    if (lp > 1024) return RGSV_ERR_DIMENSION;
+    if (lp > kCholMaxKp) return RGSV_ERR_DIMENSION;
     double* pt = nullptr;
     if (int e = cholqr3_wide(S, S2, n, lds, l, (int)lp, gram, linv, rinv, rdiag, scratch, sb,
                              status, &pt, st))
@@ -608,7 +608,7 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
   } else {
     // tall stacked matrix (l > n): Q = qr(S).q directly
     const int64_t kpn = L.kpn;
-    if (kpn > 1024) return RGSV_ERR_DIMENSION;  // blocked Cholesky limit
+    if (kpn > kCholMaxKp) return RGSV_ERR_DIMENSION;  // blocked Cholesky limit
     if (int e = launch_stack(S, kpn, b1, ldb1, l1, b2, ldb2, l2, l, n, st)) return e;
     if (int e = cholqr3_tall(S, S2, l, (int)n, (int)kpn, gram, linv, rdiag, scratch, sb, status,
                              &Q, st))

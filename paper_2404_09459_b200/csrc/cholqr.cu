@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(256) k_chol_b16(const double* __restrict__ gra
   }
 }
 
-// ------------------------------------------- blocked, 128 < kp <= 1024
+// ------------------------------------------- blocked, 128 < kp <= 4096
 // kp beyond one CTA's shared memory (cfg4: the 288-wide range-finder blocks
 // and the 576-wide stacked pair). Right-looking blocked Cholesky on a global
 // (L2-resident) working copy: each <= 128-wide diagonal block is factorised
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(256) k_chol_b16(const double* __restrict__ gra
 // padding as the one-CTA kernels.
 
 // W = gram (+ shift s I on the k real columns, identity on the padding);
-// every block recomputes the trace (k <= 1024 diagonal reads).
+// every block recomputes the trace (k <= kCholMaxKp diagonal reads).
 __global__ void k_chol_prep(const double* __restrict__ gram, int k, int kp, int64_t shift_rows,
                             double* __restrict__ W) {
   double sh = 0.0;
@@ -1042,7 +1042,7 @@ int chol_inv_blocked(const double* gram, int k, int kp, int64_t shift_rows, doub
 
 int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
              double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st) {
-  if (k <= 0 || kp < k || kp % 16 != 0 || kp > 1024) return RGSV_ERR_DIMENSION;
+  if (k <= 0 || kp < k || kp % 16 != 0 || kp > kCholMaxKp) return RGSV_ERR_DIMENSION;
   if (kp <= 64 && !getenv("RGSV_CHOL_BLK")) {
     const size_t bytes = (size_t)2 * kp * (kp + 4) * sizeof(double);
     static bool attr_b16 = false;

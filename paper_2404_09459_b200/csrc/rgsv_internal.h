@@ -32,6 +32,8 @@ int gemm_gtq(const GemmArgs& a, cudaStream_t st);
 // 11 (rows k + k (k+1)) u trace (shifted CholeskyQR, Fukaya et al. 2020);
 // writes Linv = L^{-1} (kp x kp, identity padding), optionally its
 // transpose Rinv, R = L^T, and the diagonal of R. status[0] |= 1 on breakdown.
+// kp <= 128: one CTA; up to kCholMaxKp: blocked (DMMA panels, stream-ordered scratch)
+constexpr int kCholMaxKp = 4096;
 int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv, double* rinv,
              double* r_upper, double* rdiag, double* rdiag_acc, int* status, cudaStream_t st);
 

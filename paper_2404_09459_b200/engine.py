@@ -45,14 +45,14 @@ class GmpPair:
     """A pair {g1 (m x n), g2 (p x n)} held in HBM (engine.py:31-90).
 
     Construction validates shapes, the field (real only on the B200 path),
-    finiteness (device pass) and m + p >= n. Like the reference it checks
+    finiteness (device pass) and m + p >= n, and -- like the reference --
     sigma_min > 1e-12 sigma_max of the stacked pair (engine.py:55-61), on the
-    device (validation.py). ``check_rank=None`` (default) runs that check
-    whenever it is cheap (n <= 512: every reference test shape) and skips
-    it for the larger configs, which the reference's own benchmark plan also
-    builds unvalidated; True forces it (up to n = 1024
-    through the blocked Cholesky, ~3 s at cfg1's 36000 x 1000; DimensionError
-    beyond), False skips it."""
+    device (validation.py: Householder or CholeskyQR3 R factor, then blocked
+    Jacobi). ``check_rank=None`` (default) and True both run the check; it
+    covers n <= 4096 (every reference shape and cfg0-cfg3) and raises
+    DimensionError beyond (cfg4: n = 8192), where the pair must be built
+    with check_rank=False. With False the stacked norms (stack_norm2,
+    stack_pinv_norm) are computed on first access instead."""
 
     g1: object
     g2: object
@@ -71,19 +71,23 @@ class GmpPair:
                 raise ValidationError(f"{name} contains non-finite entries")
         object.__setattr__(self, "g1", a)
         object.__setattr__(self, "g2", b)
-        check = self.check_rank
-        if check is None:
-            check = _dev.ceil16(n) <= 512 or (a.rows + b.rows) * n <= (1 << 22)
-        if check:
+        if self.check_rank is not False:
+            self._stack_norms()
+
+    def _stack_norms(self):
+        """sigma_max / sigma_min of vstack(g1, g2) (engine.py:55-61, 82-90),
+        computed once on the device; RankDeficiencyError like the reference."""
+        if not hasattr(self, "_stack_smax"):
             from .validation import stacked_extreme_singular_values
 
-            smax, smin = stacked_extreme_singular_values(a, b)
+            smax, smin = stacked_extreme_singular_values(self.g1, self.g2)
             if smin <= 1e-12 * smax:
                 raise RankDeficiencyError(
                     f"stacked pair is numerically rank deficient "
                     f"(sigma_min/sigma_max = {smin / smax if smax else 0.0:.3e})")
             object.__setattr__(self, "_stack_smax", smax)
             object.__setattr__(self, "_stack_smin", smin)
+        return self._stack_smax, self._stack_smin
 
     @classmethod
     def resident(cls, g1, g2) -> "GmpPair":
@@ -112,15 +116,13 @@ class GmpPair:
 
     @property
     def stack_norm2(self) -> float:
-        if not hasattr(self, "_stack_smax"):
-            raise AttributeError("construct with check_rank=True to compute stacked norms")
-        return self._stack_smax
+        """Largest singular value of the stacked pair (cached; engine.py:82-85)."""
+        return self._stack_norms()[0]
 
     @property
     def stack_pinv_norm(self) -> float:
-        if not hasattr(self, "_stack_smin"):
-            raise AttributeError("construct with check_rank=True to compute stacked norms")
-        return 1.0 / self._stack_smin
+        """Spectral norm of the stacked pair's pseudoinverse (engine.py:87-90)."""
+        return 1.0 / self._stack_norms()[1]
 
 
 @dataclass(frozen=True)
