@@ -236,6 +236,21 @@ int rgsv_comparative(const double* sv1, const int* nsv, const double* sv2, int64
                      double* theta, double* p1, double* p2, double* scalars, int* counts,
                      int* status, void* stream);
 
+/* engine.spectrum_from_l_blocks (engine.py:189-225) on given L blocks:
+ * singular values of L1 (l1 x cols) and L2 (l2 x cols) by one-sided
+ * Jacobi, then the completion -- branch 0 = merged (default), 1 = "first"
+ * (betas from the alphas, L2 unused), 2 = "second" -- and
+ * classify_spectrum (engine.py:164-186): alphas, betas (n), counts = {r, s}.
+ * status: RGSV_ST_JACOBI / RGSV_ST_CLASSIFY as in rgsv_small_gsvd (the
+ * DEGENERATE / NOT_NORMALIZED bits of the comparative stage are
+ * informational here). */
+size_t rgsv_spectrum_from_l_blocks_workspace_bytes(int l1, int l2, int cols, int64_t n);
+int rgsv_spectrum_from_l_blocks(const double* l1b, int64_t ld1, int l1, const double* l2b,
+                                int64_t ld2, int l2, int cols, int64_t n, double classify_tol,
+                                int branch, double* alphas, double* betas, int* counts,
+                                int* status, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
 /* Per-quantity forms of analysis.py:37-79 for a given spectrum (alphas,
  * betas, r): rho (inf for i < r), theta, p1, p2, scalars = {d1, d2, sum p1,
  * sum p2}; and D of a given probability vector (scalars[0] = D,

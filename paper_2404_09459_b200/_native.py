@@ -77,6 +77,9 @@ SIGNATURES = {
     "rgsv_dense_qr": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _i32, _p, _i64, _p, _i64, _i32, _p,
                              _sz, _p]),
     "rgsv_comparative": (_i32, [_p, _p, _p, _i64, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "rgsv_spectrum_from_l_blocks_workspace_bytes": (_sz, [_i32, _i32, _i32, _i64]),
+    "rgsv_spectrum_from_l_blocks": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _i32, _i64, _d, _i32,
+                                           _p, _p, _p, _p, _p, _sz, _p]),
     "rgsv_spectrum_quantities": (_i32, [_p, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "rgsv_entropy": (_i32, [_p, _i64, _p, _p]),
     "rgsv_svd_values_workspace_bytes": (_sz, [_i32, _i32]),

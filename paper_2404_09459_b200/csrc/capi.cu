@@ -671,6 +671,70 @@ int rgsv_comparative(const double* sv1, const int* nsv, const double* sv2, int64
                             scalars, counts, status, 0, 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
+size_t rgsv_spectrum_from_l_blocks_workspace_bytes(int l1, int l2, int cols, int64_t n) {
+  return al256((size_t)(l1 > 0 ? l1 : 1) * (cols + 1) * 8) +
+         al256((size_t)(l2 > 0 ? l2 : 1) * (cols + 1) * 8) + al256(2 * sizeof(double) * (cols + 1)) +
+         bjacobi_sync_bytes() + al256(8 * (4 * (size_t)n + 4)) + 256;
+}
+
+int rgsv_spectrum_from_l_blocks(const double* l1b, int64_t ld1, int l1, const double* l2b,
+                                int64_t ld2, int l2, int cols, int64_t n, double classify_tol,
+                                int branch, double* alphas, double* betas, int* counts,
+                                int* status, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (l1 < 0 || l2 < 0 || cols < 0 || n < 1 || branch < 0 || branch > 2) return RGSV_ERR_DIMENSION;
+  if (!(classify_tol > 0.0 && classify_tol < 1e-2)) return RGSV_ERR_VALIDATION;
+  if (workspace_bytes < rgsv_spectrum_from_l_blocks_workspace_bytes(l1, l2, cols, n))
+    return RGSV_ERR_WORKSPACE;
+  char* ws = static_cast<char*>(workspace);
+  double* v1 = reinterpret_cast<double*>(ws);
+  ws += al256((size_t)(l1 > 0 ? l1 : 1) * (cols + 1) * 8);
+  double* v2 = reinterpret_cast<double*>(ws);
+  ws += al256((size_t)(l2 > 0 ? l2 : 1) * (cols + 1) * 8);
+  double* sv = reinterpret_cast<double*>(ws);  // sv1 | sv2 (cols + 1 each... <= min dims)
+  ws += al256(2 * sizeof(double) * (cols + 1));
+  void* sync = ws;
+  ws += bjacobi_sync_bytes();
+  double* q4 = reinterpret_cast<double*>(ws);  // rho | theta | p1 | p2 | scalars (unused here)
+  ws += al256(8 * (4 * (size_t)n + 4));
+  int* nsv = reinterpret_cast<int*>(ws);
+  double* sv1 = sv;
+  double* sv2 = sv + (cols + 1);
+  // singular values of each block by one-sided Jacobi on its shorter side
+  auto orient = [&](const double* b, int64_t ldb, int rows, double* v, int* nv, int* len,
+                    int64_t* ld) -> int {
+    if (rows == 0 || cols == 0) {
+      *nv = 0;
+      *len = cols > 0 ? cols : 1;
+      *ld = *len;
+      return 0;
+    }
+    if (rows <= cols) {
+      *nv = rows;
+      *len = cols;
+      *ld = cols;
+      return launch_copy_block(v, cols, b, ldb, rows, cols, 0, st);
+    }
+    *nv = cols;
+    *len = rows;
+    *ld = rows;
+    return launch_copy_block(v, rows, b, ldb, cols, rows, 1, st);
+  };
+  int nv1, len1, nv2, len2;
+  int64_t vld1, vld2;
+  if (int e = orient(l1b, ld1, l1, v1, &nv1, &len1, &vld1)) return e;
+  if (int e = orient(l2b, ld2, branch == 1 ? 0 : l2, v2, &nv2, &len2, &vld2)) return e;
+  if (int e = jacobi_dispatch(v1, vld1, nv1, len1, sv1, nsv, v2, vld2, nv2, len2, sv2, nsv + 1,
+                              status, sync, st))
+    return e;
+  // spectrum completion (merged / forced branch) + classification; the
+  // comparative quantities the kernel also forms go to scratch
+  return launch_comparative(sv1, nsv, sv2, n, classify_tol, alphas, betas, q4, q4 + n, q4 + 2 * n,
+                            q4 + 3 * n, q4 + 4 * n, counts, status, branch == 0 ? 0 : branch + 2,
+                            0, st);
+}
+
 int rgsv_spectrum_quantities(const double* alphas, const double* betas, int64_t n, int r,
                              double* rho, double* theta, double* p1, double* p2, double* scalars,
                              int* status, void* stream) {

@@ -832,7 +832,7 @@ __device__ void comparative_body(const double* __restrict__ sv1, const int* __re
                                  double* __restrict__ rho, double* __restrict__ theta,
                                  double* __restrict__ p1, double* __restrict__ p2,
                                  double* __restrict__ scalars, int* __restrict__ counts,
-                                 int* __restrict__ status, double* red);
+                                 int* __restrict__ status, double* red, int branch = 0);
 
 __global__ void __launch_bounds__(1024) k_comparative(
     const double* __restrict__ sv1, const int* __restrict__ nsv, const double* __restrict__ sv2,
@@ -898,18 +898,20 @@ __global__ void __launch_bounds__(1024) k_comparative(
     }
     return;
   }
-  comparative_body(sv1, nsv, sv2, n, tol, A, B, rho, theta, p1, p2, scalars, counts, status, red);
+  // mode 0: merged completion (default); 3 / 4: branch "first" / "second"
+  comparative_body(sv1, nsv, sv2, n, tol, A, B, rho, theta, p1, p2, scalars, counts, status, red,
+                   mode == 3 ? 1 : (mode == 4 ? 2 : 0));
 }
 
-// spectrum completion + classification + comparative quantities (mode 0 of
-// k_comparative); whole CTA, `red` = 32 doubles of shared scratch.
+// spectrum completion + classification + comparative quantities (modes 0 /
+// 3 / 4 of k_comparative); whole CTA, `red` = 32 doubles of shared scratch.
 __device__ void comparative_body(const double* __restrict__ sv1, const int* __restrict__ nsv,
                                  const double* __restrict__ sv2, int64_t n, double tol,
                                  double* __restrict__ A, double* __restrict__ B,
                                  double* __restrict__ rho, double* __restrict__ theta,
                                  double* __restrict__ p1, double* __restrict__ p2,
                                  double* __restrict__ scalars, int* __restrict__ counts,
-                                 int* __restrict__ status, double* red) {
+                                 int* __restrict__ status, double* red, int branch) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t c1 = nsv[0], c2 = nsv[1];
   double cr = 0.0, cza = 0.0;
@@ -918,8 +920,15 @@ __device__ void comparative_body(const double* __restrict__ sv1, const int* __re
     const double br = (i >= n - c2) ? fmin(fmax(sv2[n - 1 - i], 0.0), 1.0) : 0.0;
     double a, b;
     // numpy evaluates sqrt(1.0 - x**2) with two roundings; keep them
-    // (no FMA contraction) so the completed spectrum matches bit for bit
-    if (ar <= br) {
+    // (no FMA contraction) so the completed spectrum matches bit for bit.
+    // branch 1 / 2 force the one-sided completion of engine.py:211-219.
+    if (branch == 1) {
+      a = ar;
+      b = sqrt(__dsub_rn(1.0, __dmul_rn(ar, ar)));
+    } else if (branch == 2) {
+      a = sqrt(__dsub_rn(1.0, __dmul_rn(br, br)));
+      b = br;
+    } else if (ar <= br) {
       a = ar;
       b = sqrt(__dsub_rn(1.0, __dmul_rn(ar, ar)));
     } else {

@@ -20,6 +20,8 @@ import torch
 from . import device as _dev
 from . import tf32 as _tf32
 from ._native import ST_CHOL, ST_CLASSIFY, ST_JACOBI, ST_OMEGA_SHORT
+from ._native import check as _check
+from ._native import lib as _native_lib
 from .errors import (
     ConvergenceError,
     DimensionError,
@@ -213,6 +215,122 @@ def classify_spectrum(alphas, betas, classify_tol: float = 1e-10) -> tuple[int, 
         a[n - za:] = 0.0
         b[n - za:] = 1.0
     return r, s
+
+
+def spectrum_from_l_blocks(l1_block, l2_block, n: int, classify_tol: float = 1e-10,
+                           branch: str | None = None) -> GsvSpectrum:
+    """GSVs read off the stacked-QR orthonormal blocks (engine.py:189-225)
+    on the device: one-sided Jacobi singular values of both blocks, clamp to
+    [0, 1], the merged completion (each index keeps its smaller member and
+    completes the other through sqrt(1 - x^2)) or the forced one-sided
+    ``branch`` ("first" / "second"), then classify_spectrum's counts and
+    snapping (engine.py:164-186) -- rgsv_spectrum_from_l_blocks, one call."""
+    if branch not in (None, "first", "second"):
+        raise ValidationError(f"branch must be None, 'first' or 'second', got {branch!r}")
+    if not 0 < classify_tol < 1e-2:
+        raise ValidationError(f"classify_tol must be in (0, 1e-2), got {classify_tol}")
+    blocks = []
+    for name, blk in (("l1_block", l1_block), ("l2_block", l2_block)):
+        if isinstance(blk, torch.Tensor):
+            t = blk.to(device="cuda", dtype=torch.float64)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(np.asarray(blk, dtype=np.float64))).cuda()
+        if t.dim() != 2:
+            raise DimensionError(f"{name} must be 2-D")
+        blocks.append(t.contiguous())
+    b1, b2 = blocks
+    l1, c1 = b1.shape
+    l2, c2 = b2.shape
+    if l1 and l2 and c1 != c2:
+        raise DimensionError(f"L blocks have {c1} and {c2} columns")
+    cols = c1 if l1 else c2
+    L = _native_lib()
+    nb = int(L.rgsv_spectrum_from_l_blocks_workspace_bytes(l1, l2, cols, n))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    alphas = torch.empty(n, dtype=torch.float64, device="cuda")
+    betas = torch.empty(n, dtype=torch.float64, device="cuda")
+    ints = torch.zeros(3, dtype=torch.int32, device="cuda")
+    dummy = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _check(L.rgsv_spectrum_from_l_blocks(
+        _dev.vp(b1 if l1 else dummy), max(c1, 1), l1, _dev.vp(b2 if l2 else dummy), max(c2, 1), l2,
+        cols, n, classify_tol, {None: 0, "first": 1, "second": 2}[branch], _dev.vp(alphas),
+        _dev.vp(betas), _dev.vp(ints[:2]), _dev.vp(ints[2:]), _dev.vp(ws), nb,
+        _dev.sp(torch.cuda.current_stream())), "rgsv_spectrum_from_l_blocks")
+    r, s, status = (int(x) for x in ints.cpu())
+    if status & ST_JACOBI:
+        raise ConvergenceError("Jacobi SVD of an L block did not converge")
+    if status & ST_CLASSIFY:
+        raise ValidationError("overlapping zero classifications; sequences not ordered?")
+    return GsvSpectrum(alphas.cpu().numpy(), betas.cpu().numpy(), r, s)
+
+
+@dataclass(frozen=True)
+class _Pipeline:
+    """The reference's internal pipeline record (engine.py:234-242): bases
+    (None for method="direct"), the stacked-QR L blocks, R-tilde and the
+    BasisResults. Host arrays, as the reference returns them."""
+
+    q1: np.ndarray | None
+    q2: np.ndarray | None
+    l1_block: np.ndarray
+    l2_block: np.ndarray
+    r_tilde: np.ndarray
+    basis1: object | None = None
+    basis2: object | None = None
+
+
+def _run_pipeline(pair: GmpPair, opts: GsvOptions) -> _Pipeline:
+    """engine._run_pipeline (engine.py:245-261) on the device -- the seam the
+    reference's bench._timed_run (bench.py:74) and cli._cmd_bounds
+    (cli.py:163) call: bases (extract_basis on the device, G2 with seed + 1),
+    C_i = Q_i^T G_i (DMMA), the stacked reduced QR [C1; C2] = Q R-tilde
+    (multi-CTA Householder for <= 1408 stacked rows, CholeskyQR3 above) with
+    the reference's phase convention, L blocks = row blocks of Q."""
+    from .core import HH_MAX_ROWS, _gemm_at_b, dense_qr, tall_qr
+
+    if pair.g1.is_f32 or pair.g2.is_f32:
+        pair = _promoted(pair)
+    n = pair.n
+    if opts.method == DIRECT:
+        c1, c2 = pair.g1.t, pair.g2.t
+        q1 = q2 = None
+        b1 = b2 = None
+    else:
+        from .rangefinder import extract_basis
+
+        cfg = opts.extraction
+        b1 = extract_basis(pair.g1, cfg)
+        b2 = extract_basis(pair.g2, dataclasses.replace(cfg, seed=cfg.seed + 1))
+        q1, q2 = b1.q, b2.q
+        cs = []
+        for q, g in ((q1, pair.g1), (q2, pair.g2)):
+            w = q.shape[1]
+            if w == 0:
+                cs.append(torch.zeros((0, n), dtype=torch.float64, device="cuda"))
+                continue
+            qd = torch.zeros((g.rows, _dev.ceil16(w)), dtype=torch.float64, device="cuda")
+            qd[:, :w] = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+            cs.append(_gemm_at_b(qd, g.t, w, n, g.rows))
+        c1, c2 = cs
+    l1, l2 = c1.shape[0], c2.shape[0]
+    l = l1 + l2
+    if l == 0:
+        raise RankDeficiencyError("both compressed blocks are empty")
+    if l <= HH_MAX_ROWS:
+        if l1 and l2:
+            q, r = dense_qr(c1, l1, c2, l2, n)
+        else:
+            q, r = dense_qr(c1 if l1 else c2, l, None, 0, n)
+    elif l >= n:
+        s_ = torch.zeros((l, n + (n & 1)), dtype=torch.float64, device="cuda")
+        s_[:l1, :n] = c1
+        s_[l1:, :n] = c2
+        q, r = tall_qr(s_[:, :n], l, n)
+    else:
+        raise DimensionError(f"stacked reduced QR of a wide {l} x {n} block with more than "
+                             f"{HH_MAX_ROWS} rows is not supported")
+    qh = q.cpu().numpy()
+    return _Pipeline(q1, q2, qh[:l1], qh[l1:], r.cpu().numpy(), b1, b2)
 
 
 @dataclass
@@ -624,6 +742,7 @@ def recover_gsvd(pair: GmpPair, opts: GsvOptions | None = None) -> GsvdFactors:
 
 
 __all__ = ["GmpPair", "GsvSpectrum", "GsvOptions", "GsvdFactors", "classify_spectrum",
+           "spectrum_from_l_blocks",
            "compute_gsv", "compute_gsv_batch", "recover_gsvd", "run_device_pipeline",
            "run_device_batch", "RANDOMIZED", "DIRECT",
            "dataclasses"]
