@@ -628,12 +628,16 @@ def fp64_gemm_roofline(cfg, gmat, rows: int, steps_time_per_pair: float, world: 
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = dv.sp(torch.cuda.current_stream())
 
+    # the chain runs the exact-width (120-wide) tiles when k = 120 (cfg2):
+    # time the same kernels by asking for exactly the live width
+    kl = cfg.k if cfg.k == 120 else kp
+
     def gtq():
-        L.rgsv_gemm_gtq(dv.vp(Q), kp, dv.vp(gmat.t), gmat.ld, dv.vp(Bo), ldb, kp, cfg.n, rows,
+        L.rgsv_gemm_gtq(dv.vp(Q), kp, dv.vp(gmat.t), gmat.ld, dv.vp(Bo), ldb, kl, cfg.n, rows,
                         dv.vp(scratch), scratch.numel(), st)
 
     def gx():
-        L.rgsv_gemm_gx(dv.vp(gmat.t), gmat.ld, dv.vp(Xt), ldb, dv.vp(Y), kp, rows, kp, cfg.n,
+        L.rgsv_gemm_gx(dv.vp(gmat.t), gmat.ld, dv.vp(Xt), ldb, dv.vp(Y), kp, rows, kl, cfg.n,
                        dv.vp(scratch), scratch.numel(), st)
 
     t_gtq = time_kernel(gtq)

@@ -369,6 +369,7 @@ int rgsv_sketch_project_sharded(const double* g, int64_t ldg, int64_t m, int64_t
   s.ldc = kp;
   s.M = m;
   s.N = kp;
+  s.live = k;  // exact-width tiles where they exist (k = 120: cfg2)
   s.K = n;
   s.scratch = scratch;
   s.scratch_bytes = sb;
@@ -401,6 +402,7 @@ int rgsv_sketch_project_sharded(const double* g, int64_t ldg, int64_t m, int64_t
     p.ldc = ldn;
     p.M = kp;
     p.N = n;
+    p.live = k;
     p.K = m;
     p.scratch = scratch;
     p.scratch_bytes = sb;
@@ -431,6 +433,7 @@ int rgsv_sketch_project_sharded(const double* g, int64_t ldg, int64_t m, int64_t
   p.ldc = ldb;
   p.M = kp;
   p.N = n;
+  p.live = k;
   p.K = m;
   p.scratch = scratch;
   p.scratch_bytes = sb;

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     k_gx(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX,
          double* __restrict__ out, int64_t ld_out, double* __restrict__ part,
          int64_t part_stride, int part_row0, int M, int N, Decomp d,
-         double* __restrict__ ss_out) {
+         double* __restrict__ ss_out, int zero_to) {
   constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN, NCW = WM * WN;
   constexpr uint32_t G_BYTES = BM * 128, X_BYTES = BN * 128, STAGE = G_BYTES + X_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -161,6 +161,15 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
         p[0] = acc[mt][nt][0];
       }
     }
+    // exact-width variant: the padding columns [N, zero_to) of the output
+    // (never multiplied) are stored as zeros, straight to `out`
+    if (zero_to > N && wn == WN - 1 && tn == d.tiles_n - 1) {
+      double* zr = out + (int64_t)row * ld_out;
+      for (int col = N + 2 * t; col < zero_to; col += 8) {
+        zr[col] = 0.0;
+        if (col + 1 < zero_to) zr[col + 1] = 0.0;
+      }
+    }
   }
   if (SUMSQ) {
     ss = warp_sum(ss);
@@ -179,10 +188,13 @@ template <int MT, int NT, int WM, int WN, int STAGES, int MINB = 1>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     k_gtq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmG,
           double* __restrict__ out, int64_t ld_out, double* __restrict__ part,
-          int64_t part_stride, int Mk, int N, Decomp d) {
+          int64_t part_stride, int Mk, int N, Decomp d, int zero_to) {
   constexpr int BM = MT * 8 * WM, BN = NT * 8 * WN, NCW = WM * WN;
-  constexpr int QBOX = BM / 16, GBOX = BN / 16;
-  constexpr uint32_t Q_BYTES = BM * 128, G_BYTES = BN * 128, STAGE = Q_BYTES + G_BYTES;
+  // Q is staged in 16-column boxes: an exact-width BM (120) stages 128
+  // columns (the OOB tail is zero-filled by TMA) and multiplies BM of them
+  constexpr int QBOX = (BM + 15) / 16, GBOX = BN / 16;
+  static_assert(BN % 16 == 0, "G tile width must be whole 16-column boxes");
+  constexpr uint32_t Q_BYTES = QBOX * 2048, G_BYTES = BN * 128, STAGE = Q_BYTES + G_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -262,6 +274,21 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
   }
 
   double* o = split < 0 ? out : part + split * part_stride;
+  // exact-width variant: output rows [Mk, zero_to) (never multiplied) are
+  // stored as zeros, straight to `out`
+  if (zero_to > Mk && wm == 0 && tk == 0) {
+    for (int row = Mk + g; row < zero_to; row += 8)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int col = n0 + (wn * NT + nt) * 8 + 2 * t;
+        double* p = out + (int64_t)row * ld_out + col;
+        if (col + 1 < N) {
+          *reinterpret_cast<double2*>(p) = make_double2(0.0, 0.0);
+        } else if (col < N) {
+          p[0] = 0.0;
+        }
+      }
+  }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int row = k0 + (wm * MT + mt) * 8 + g;
@@ -320,6 +347,15 @@ static int reduce_blocks(int64_t total) {
 
 // -------------------------------------------------------------- host side
 namespace {
+
+// RGSV_EXACT_WIDTH=0 turns the exact-width (k = 120) tiles off (A/B runs).
+bool exact_width_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RGSV_EXACT_WIDTH");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
 
 template <typename K>
 int set_smem(K kernel, size_t bytes) {
@@ -395,7 +431,8 @@ int run_gx(const GemmArgs& a, cudaStream_t st) {
   auto kern = k_gx<MT, NT, WM, WN, STAGES, SUMSQ, MINB>;
   if (int e = set_smem(kern, smem)) return e;
   kern<<<units, (WM * WN + 1) * 32, smem, st>>>(tmG, tmX, a.C, a.ldc, a.scratch, part_stride,
-                                                 part_row0, (int)a.M, (int)a.N, d, a.ss_out);
+                                                 part_row0, (int)a.M, (int)a.N, d, a.ss_out,
+                                                 a.zero_to);
   note_launch();
   if (S > 0) {
     const int rows = (int)(a.M - part_row0);
@@ -442,6 +479,11 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
       }
     }
   }
+  // never more partials than the caller's scratch holds
+  const size_t per_split = (size_t)a.M * a.ldc * sizeof(double);
+  if (split > 1 && (size_t)split * per_split > a.scratch_bytes)
+    split = per_split ? (int)(a.scratch_bytes / per_split) : 1;
+  if (split < 1) split = 1;
   int units = tiles, S = 0;
   if (split == 1) {
     d.full = tiles;
@@ -459,11 +501,11 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
     if (need > a.scratch_bytes) return RGSV_ERR_WORKSPACE;
   }
   const int64_t part_stride = (int64_t)a.M * a.ldc;
-  const size_t smem = STAGES * (BM + BN) * 128 + 2 * STAGES * 8 + 1024;
+  const size_t smem = STAGES * (((BM + 15) / 16) * 16 + BN) * 128 + 2 * STAGES * 8 + 1024;
   auto kern = k_gtq<MT, NT, WM, WN, STAGES, MINB>;
   if (int e = set_smem(kern, smem)) return e;
   kern<<<units, (WM * WN + 1) * 32, smem, st>>>(tmQ, tmG, a.C, a.ldc, a.scratch, part_stride,
-                                                 (int)a.M, (int)a.N, d);
+                                                 (int)a.M, (int)a.N, d, a.zero_to);
   note_launch();
   if (S > 0) {
     const int blocks = reduce_blocks((int64_t)a.M * a.N);
@@ -477,8 +519,19 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
 }  // namespace
 
 // C (M x N) = A (M x K) * B^T  with B given as N x K (both K-major).
-int gemm_gx(const GemmArgs& a, cudaStream_t st) {
-  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return RGSV_ERR_DIMENSION;
+// a.live (> 0): only the first `live` output columns can be nonzero (the
+// rest of B^T is zero padding); a live width of 120 in a 128-wide output
+// (cfg2's k) runs the exact-width tile and zero-fills columns 120..127.
+int gemm_gx(const GemmArgs& a0, cudaStream_t st) {
+  if (a0.M <= 0 || a0.N <= 0 || a0.K <= 0) return RGSV_ERR_DIMENSION;
+  if (exact_width_enabled() && (a0.N == 120 || (a0.live == 120 && a0.N == 128))) {
+    GemmArgs a = a0;
+    a.zero_to = a0.N;  // 128: zero-fill the padding columns
+    a.N = 120;
+    if (a.ss_out) return run_gx<2, 15, 8, 1, 5, true>(a, st);
+    return run_gx<2, 15, 8, 1, 5, false>(a, st);
+  }
+  const GemmArgs& a = a0;
   if (a.ss_out) {
     if (a.N <= 16) return run_gx<2, 2, 8, 1, 6, true>(a, st);
     if (a.N <= 32) return run_gx<2, 4, 8, 1, 6, true>(a, st);
@@ -493,8 +546,21 @@ int gemm_gx(const GemmArgs& a, cudaStream_t st) {
 }
 
 // C (M x N) = A^T * B with A: K x M, B: K x N (both row-major, reduction over K rows).
-int gemm_gtq(const GemmArgs& a, cudaStream_t st) {
-  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return RGSV_ERR_DIMENSION;
+// a.live (> 0): only the first `live` output rows can be nonzero (the rest
+// of A's columns are zero padding); live 120 of M 128 runs the exact-width
+// 120 x 64 tile (8 DMMA warps, each 120 x 8; a 9-warp 120 x 96 tile
+// measured 15% slower -- 9 warps split 3/2/2/2 over the 4 SM sub-partitions
+// -- and 120 x 16 per warp spills at the 168-register cap) and zero-fills
+// rows 120..127.
+int gemm_gtq(const GemmArgs& a0, cudaStream_t st) {
+  if (a0.M <= 0 || a0.N <= 0 || a0.K <= 0) return RGSV_ERR_DIMENSION;
+  if (exact_width_enabled() && a0.N > 128 && (a0.M == 120 || (a0.live == 120 && a0.M == 128))) {
+    GemmArgs a = a0;
+    a.zero_to = a0.M;  // 128: zero-fill the padding rows
+    a.M = 120;
+    return run_gtq<15, 1, 1, 8, 6>(a, st);
+  }
+  const GemmArgs& a = a0;
   if (a.N <= 16 && a.M <= 16) return run_gtq<1, 1, 2, 2, 6>(a, st);
   if (a.N <= 32 && a.M <= 32) return run_gtq<2, 2, 2, 2, 6>(a, st);
   if (a.N <= 64 && a.M <= 64) return run_gtq<4, 4, 2, 2, 6>(a, st);

@@ -23,6 +23,8 @@ struct GemmArgs {
   int max_split = 32;
   double* ss_out = nullptr;  // gx only: per-unit sum of squares of A
   int* ss_units = nullptr;
+  int live = 0;     // output columns (gx) / rows (gtq) that can be nonzero; 0 = all
+  int zero_to = 0;  // internal: padding [N or M, zero_to) stored as zeros
 };
 
 int gemm_gx(const GemmArgs& a, cudaStream_t st);
