@@ -521,15 +521,17 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
 // C (M x N) = A (M x K) * B^T  with B given as N x K (both K-major).
 // a.live (> 0): only the first `live` output columns can be nonzero (the
 // rest of B^T is zero padding); a live width of 120 in a 128-wide output
-// (cfg2's k) runs the exact-width tile and zero-fills columns 120..127.
+// (cfg2's k) runs the exact-width 128 x 120 tile and zero-fills columns
+// 120..127. 12 DMMA warps of 32 x 40 (3 per SM sub-partition): 5603 us at
+// cfg2 vs 5894 us for 8 warps of 16 x 120 and 6126 us for the padded tile.
 int gemm_gx(const GemmArgs& a0, cudaStream_t st) {
   if (a0.M <= 0 || a0.N <= 0 || a0.K <= 0) return RGSV_ERR_DIMENSION;
   if (exact_width_enabled() && (a0.N == 120 || (a0.live == 120 && a0.N == 128))) {
     GemmArgs a = a0;
     a.zero_to = a0.N;  // 128: zero-fill the padding columns
     a.N = 120;
-    if (a.ss_out) return run_gx<2, 15, 8, 1, 5, true>(a, st);
-    return run_gx<2, 15, 8, 1, 5, false>(a, st);
+    if (a.ss_out) return run_gx<4, 5, 4, 3, 5, true>(a, st);
+    return run_gx<4, 5, 4, 3, 5, false>(a, st);
   }
   const GemmArgs& a = a0;
   if (a.ss_out) {
@@ -548,17 +550,17 @@ int gemm_gx(const GemmArgs& a0, cudaStream_t st) {
 // C (M x N) = A^T * B with A: K x M, B: K x N (both row-major, reduction over K rows).
 // a.live (> 0): only the first `live` output rows can be nonzero (the rest
 // of A's columns are zero padding); live 120 of M 128 runs the exact-width
-// 120 x 64 tile (8 DMMA warps, each 120 x 8; a 9-warp 120 x 96 tile
-// measured 15% slower -- 9 warps split 3/2/2/2 over the 4 SM sub-partitions
-// -- and 120 x 16 per warp spills at the 168-register cap) and zero-fills
-// rows 120..127.
+// 120 x 64 tile (12 DMMA warps of 40 x 16, 3 per SM sub-partition) and
+// zero-fills rows 120..127. Measured at cfg2: 6125 us vs 6234 us for 8 warps
+// of 120 x 8 and 6579 us for the padded 128-row tile; a 9-warp 120 x 96 tile
+// ran 7559 us (9 warps split 3/2/2/2 over the 4 sub-partitions).
 int gemm_gtq(const GemmArgs& a0, cudaStream_t st) {
   if (a0.M <= 0 || a0.N <= 0 || a0.K <= 0) return RGSV_ERR_DIMENSION;
   if (exact_width_enabled() && a0.N > 128 && (a0.M == 120 || (a0.live == 120 && a0.M == 128))) {
     GemmArgs a = a0;
     a.zero_to = a0.M;  // 128: zero-fill the padding rows
     a.M = 120;
-    return run_gtq<15, 1, 1, 8, 6>(a, st);
+    return run_gtq<5, 2, 3, 4, 6>(a, st);
   }
   const GemmArgs& a = a0;
   if (a.N <= 16 && a.M <= 16) return run_gtq<1, 1, 2, 2, 6>(a, st);
