@@ -1140,6 +1140,10 @@ int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram,
     g.scratch = scratch;
     g.scratch_bytes = scratch_bytes;
     g.max_split = tall_gram_split();
+    if (k == 120 && kp == 128) {  // exact-width Gram (cfg2): the 120 x 120 live block
+      g.live = 120;
+      g.N = 120;
+    }
     if (int e = gemm_gtq(g, st)) return e;
     if (red)  // sum the Gram partials of every rank's row block
       if (int e = (*red)(gram, (int64_t)kp * kp, st)) return e;
@@ -1159,6 +1163,7 @@ int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram,
     t.scratch = scratch;
     t.scratch_bytes = scratch_bytes;
     t.max_split = 1;
+    t.live = k;  // exact-width TRSM tile where one exists (k = 120)
     if (int e = gemm_gx(t, st)) return e;
     double* sw = src;
     src = dst;

@@ -556,7 +556,7 @@ int gemm_gx(const GemmArgs& a0, cudaStream_t st) {
 // ran 7559 us (9 warps split 3/2/2/2 over the 4 sub-partitions).
 int gemm_gtq(const GemmArgs& a0, cudaStream_t st) {
   if (a0.M <= 0 || a0.N <= 0 || a0.K <= 0) return RGSV_ERR_DIMENSION;
-  if (exact_width_enabled() && a0.N > 128 && (a0.M == 120 || (a0.live == 120 && a0.M == 128))) {
+  if (exact_width_enabled() && a0.N >= 64 && (a0.M == 120 || (a0.live == 120 && a0.M == 128))) {
     GemmArgs a = a0;
     a.zero_to = a0.M;  // 128: zero-fill the padding rows
     a.M = 120;
