@@ -813,10 +813,12 @@ def run_ours(args, rank, world):
 
     cfg = CONFIGS[args.config]
     # concurrent pairs per step: 64 for the tiny cfg0 pairs, 8 for cfg1,
-    # one genome-scale cfg2 pair (11.2 GB)
-    # (cfg0: 6483 / 7114 / 7863 pairs/s at 8 / 32 / 64 concurrent pairs)
+    # two genome-scale cfg2 pairs (2 x 11.2 GB)
+    # (cfg0: 6483 / 7114 / 7863 pairs/s at 8 / 32 / 64 concurrent pairs;
+    #  cfg2: 14.14 / 14.66 / 14.71 pairs/s and e2e 4.18 / 4.53 / 4.69 at 1 / 2 / 3)
     B = max(1, args.batch or (64 if cfg.g_bytes * 64 <= 1e9 else
-                              8 if cfg.g_bytes * 8 <= 24e9 else 1))
+                              8 if cfg.g_bytes * 8 <= 24e9 else
+                              2 if cfg.g_bytes * 2 <= 24e9 else 1))
     hosts = [make_pair(cfg, data_seed=cfg.data_seed + rank * B + b) for b in range(B)]
     pairs = [rg.GmpPair.resident(torch.from_numpy(h1).cuda(), torch.from_numpy(h2).cuda())
              for h1, h2 in hosts]
