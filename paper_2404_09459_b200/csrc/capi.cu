@@ -500,13 +500,15 @@ int env_int(const char* name, int dflt) {
 // Stacked sizes l served by the multi-CTA Householder (k_hhqr) rather than
 // the one-CTA register kernel, and vector counts served by the blocked
 // Jacobi (k_bjacobi) rather than the one-CTA Jacobi (measured crossovers,
-// DESIGN.md §4b; RGSV_HH_MIN / RGSV_BJ_MIN override them).
+// DESIGN.md §4b; RGSV_HH_MIN / RGSV_BJ_MIN override them). Below 64 vectors
+// the one-CTA Jacobi wins in throughput: with 8 concurrent cfg1 pairs (60
+// vectors) the blocked kernel's spinning CTAs cost 736 -> 694 pairs/s.
 int hh_min_l() {
   static const int v = env_int("RGSV_HH_MIN", 129);
   return v;
 }
 int bj_min_nv() {
-  static const int v = env_int("RGSV_BJ_MIN", 33);
+  static const int v = env_int("RGSV_BJ_MIN", 64);
   return v;
 }
 }  // namespace

@@ -23,6 +23,7 @@
 // counters are zeroed by a memset node in the same stream), so they are
 // graph-capturable and need no host round trips between sweeps or panels.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "rgsv_internal.h"
@@ -682,8 +683,20 @@ size_t hhqr_workspace_bytes(int M, int N) {
   return (size_t)M * lda * 8 + npan * 32 * 33 * 8 + 1024;
 }
 
+// Grid-barrier kernels launch cooperatively (all CTAs co-resident) when the
+// grid is large. Small grids (<= kPlainGrid CTAs, one per SM) launch plainly:
+// a cooperative launch holds back concurrent work on other streams (cfg1
+// with 8 concurrent pairs: 694 vs 736 pairs/s), and a few CTAs always become
+// resident as the (finite) kernels of the other streams retire, so the
+// barrier cannot deadlock. RGSV_COOP_ALL=1 forces cooperative launches.
+constexpr int kPlainGrid = 32;
+
 static int coop_launch(const void* fn, int grid, int threads, size_t smem, void** args,
                        cudaStream_t st) {
+  static const bool coop_all = [] {
+    const char* e = getenv("RGSV_COOP_ALL");
+    return e && atoi(e) != 0;
+  }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -693,7 +706,7 @@ static int coop_launch(const void* fn, int grid, int threads, size_t smem, void*
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (coop_all || grid > kPlainGrid) ? 1 : 0;
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return RGSV_ERR_CUDA;
   note_launch();
   return 0;
