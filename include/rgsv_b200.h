@@ -312,6 +312,12 @@ int rgsv_tf32_config(int bk_gx, int bk_gtq, int rows_per_split, int flush);
 int rgsv_gemm_gx(const double* a, int64_t lda, const double* bt, int64_t ldb, double* c,
                  int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
                  size_t scratch_bytes, void* stream);
+/* Lower triangle (incl. the diagonal) of the Gram C = A^T A (A: rows x
+ * cols, row-major, ld lda; C: cols x cols, ld ldc) on the DMMA engine,
+ * skipping the output tiles strictly above the diagonal (the CholeskyQR
+ * Grams; entries of skipped tiles are left untouched). */
+int rgsv_gemm_gram_lower(const double* a, int64_t lda, int64_t cols, int64_t rows, double* c,
+                         int64_t ldc, void* scratch, size_t scratch_bytes, void* stream);
 int rgsv_gemm_gtq(const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
                   int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
                   size_t scratch_bytes, void* stream);

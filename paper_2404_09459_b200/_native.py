@@ -85,6 +85,7 @@ SIGNATURES = {
     "rgsv_svd_values_workspace_bytes": (_sz, [_i32, _i32]),
     "rgsv_svd_values": (_i32, [_p, _i64, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "rgsv_gemm_gx": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
+    "rgsv_gemm_gram_lower": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _sz, _p]),
     "rgsv_gemm_gtq": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "rgsv_chol_inv": (_i32, [_p, _i32, _i32, _i64, _p, _p, _p, _p, _p]),
     "rgsv_debug_householder_profile": (_i32, [_p, _i64, _i32, _p, _i64, _i32, _p, _i64, _p, _p]),

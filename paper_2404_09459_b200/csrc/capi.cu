@@ -799,6 +799,25 @@ int rgsv_gemm_gx(const double* a, int64_t lda, const double* bt, int64_t ldb, do
   return gemm_gx(g, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int rgsv_gemm_gram_lower(const double* a, int64_t lda, int64_t cols, int64_t rows, double* c,
+                         int64_t ldc, void* scratch, size_t scratch_bytes, void* stream) {
+  GemmArgs g;
+  g.A = a;
+  g.lda = lda;
+  g.B = a;
+  g.ldb = lda;
+  g.C = c;
+  g.ldc = ldc;
+  g.M = cols;
+  g.N = cols;
+  g.K = rows;
+  g.scratch = static_cast<double*>(scratch);
+  g.scratch_bytes = scratch_bytes;
+  g.max_split = kSMs;
+  g.lower_only = 1;
+  return gemm_gtq(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int rgsv_gemm_gtq(const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
                   int64_t ldc, int64_t M, int64_t N, int64_t K, void* scratch,
                   size_t scratch_bytes, void* stream) {

@@ -1144,6 +1144,7 @@ int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram,
       g.live = 120;
       g.N = 120;
     }
+    g.lower_only = kp > 128;  // the blocked Cholesky reads only the lower triangle
     if (int e = gemm_gtq(g, st)) return e;
     if (red)  // sum the Gram partials of every rank's row block
       if (int e = (*red)(gram, (int64_t)kp * kp, st)) return e;

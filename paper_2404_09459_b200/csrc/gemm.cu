@@ -25,6 +25,8 @@
 
 namespace rgsv {
 
+constexpr int kMaxTileMap = 64;
+
 struct Decomp {
   int tiles_n;      // tiles along the output's N dimension
   int full;         // units [0, full): tile = u, whole K range
@@ -32,6 +34,8 @@ struct Decomp {
   int split;        // splits per tail tile
   int nchunks;      // 16-deep K chunks
   int cps;          // chunks per split
+  int nmap;         // > 0: unit tiles index tmap (a lower-triangular Gram's tiles)
+  short tmap[kMaxTileMap];
 };
 
 RGSV_DI void decode_unit(const Decomp& d, int u, int& tile, int& c0, int& c1, int& s) {
@@ -48,6 +52,7 @@ RGSV_DI void decode_unit(const Decomp& d, int u, int& tile, int& c0, int& c1, in
     c1 = min(d.nchunks, c0 + d.cps);
     if (c1 < c0) c1 = c0;
   }
+  if (d.nmap > 0) tile = d.tmap[tile];
 }
 
 // ------------------------------------------------------------------- gx
@@ -313,7 +318,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
 __global__ void __launch_bounds__(256) k_reduce_splits(double* __restrict__ out, int64_t ld,
                                                        const double* __restrict__ part,
                                                        int64_t part_stride, int S, int rows,
-                                                       int cols) {
+                                                       int cols, int lower_bm = 0,
+                                                       int lower_bn = 0) {
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t total = (int64_t)rows * cols;
@@ -321,7 +327,11 @@ __global__ void __launch_bounds__(256) k_reduce_splits(double* __restrict__ out,
     const int64_t e = base + lane;
     double acc = 0.0;
     int64_t off = 0;
-    if (e < total) {
+    // lower-triangular Gram: entries of skipped (strictly upper) tiles are
+    // left untouched
+    const bool live = e < total && (lower_bm == 0 || (int)(e % cols) / lower_bn * lower_bn <
+                                                        ((int)(e / cols) / lower_bm + 1) * lower_bm);
+    if (live) {
       off = (e / cols) * ld + (e % cols);
       const double* p = part + off;
 #pragma unroll 4
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(256) k_reduce_splits(double* __restrict__ out,
     }
     red[grp][lane] = acc;
     __syncthreads();
-    if (grp == 0 && e < total) {
+    if (grp == 0 && live) {
       double t = 0.0;
 #pragma unroll
       for (int g2 = 0; g2 < 8; ++g2) t += red[g2][lane];
@@ -454,10 +464,22 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
   if (make_tmap_2d(&tmG, a.B, a.N, a.K, a.ldb, 16, 16, 8)) return RGSV_ERR_CUDA;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int nchunks = (int)((a.K + 15) / 16);
-  const int tiles = tiles_m * tiles_n;
+  int tiles = tiles_m * tiles_n;
   Decomp d{};
   d.tiles_n = tiles_n;
   d.nchunks = nchunks;
+  // a.lower_only: only tiles touching the lower triangle (n0 < m0 + BM)
+  bool lower = false;
+  if (a.lower_only && tiles <= kMaxTileMap) {
+    int nm = 0;
+    for (int t = 0; t < tiles; ++t)
+      if ((t % tiles_n) * BN < (t / tiles_n + 1) * BM) d.tmap[nm++] = (short)t;
+    if (nm < tiles) {
+      d.nmap = nm;
+      tiles = nm;
+      lower = true;
+    }
+  }
   int split = kSMs * MINB / tiles;
   if (split > a.max_split) split = a.max_split;
   if (split > nchunks) split = nchunks;
@@ -510,7 +532,7 @@ int run_gtq(const GemmArgs& a, cudaStream_t st) {
   if (S > 0) {
     const int blocks = reduce_blocks((int64_t)a.M * a.N);
     k_reduce_splits<<<blocks, 256, 0, st>>>(a.C, a.ldc, a.scratch, part_stride, S, (int)a.M,
-                                            (int)a.N);
+                                            (int)a.N, lower ? BM : 0, lower ? BN : 0);
     note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;

@@ -25,6 +25,7 @@ struct GemmArgs {
   int* ss_units = nullptr;
   int live = 0;     // output columns (gx) / rows (gtq) that can be nonzero; 0 = all
   int zero_to = 0;  // internal: padding [N or M, zero_to) stored as zeros
+  int lower_only = 0;  // gtq Gram A^T A: only tiles touching the lower triangle
 };
 
 int gemm_gx(const GemmArgs& a, cudaStream_t st);

@@ -123,6 +123,15 @@ class _Ops:
         """out (M x N) = A^T B with A: K x M, B: K x N."""
         self._gemm(self.L.rgsv_gemm_gtq, "gemm_gtq", a, lda, b, ldb, out, ldc, M, N, K)
 
+    def gram(self, a, lda, kp, rows, out):
+        """out (kp x kp) = A^T A: the lower triangle, on the tiles that touch
+        it (rgsv_gemm_gram_lower) when kp > 128 (the blocked Cholesky reads
+        only the lower part); the full product otherwise."""
+        if kp > 128:
+            self._gemm(self.L.rgsv_gemm_gram_lower, "gemm_gram_lower", a, lda, kp, rows, out, kp)
+        else:
+            self.gtq(a, lda, a, lda, out, kp, kp, kp, rows)
+
     def chol(self, gram, k, kp, shift_rows):
         linv = torch.zeros(kp * kp + kp * (kp + 1), dtype=torch.float64, device="cuda")
         rinv = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")

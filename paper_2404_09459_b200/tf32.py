@@ -124,7 +124,7 @@ def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, fina
 
     # pass 1
     gram = torch.zeros((kp, kp), dtype=f64, device="cuda")
-    ops.gtq(_dev.vp(y), kp, _dev.vp(y), kp, _dev.vp(gram), kp, kp, kp, m)
+    ops.gram(_dev.vp(y), kp, kp, m, _dev.vp(gram))
     linv, _ = ops.chol(reduce(gram), k, kp, rows_total or m)
     yh, yl = t.split_small(y, m, kp, kp)
     q1 = trsm_tc(yh, yl, linv)
@@ -145,7 +145,7 @@ def cholqr_mixed(ops, t: TF32Ops, y: torch.Tensor, m: int, k: int, kp: int, fina
     # absolute error), the identity part exact in fp64 -- the fp64 DMMA TRSM
     # took 6.9 ms on cfg4's 1e6 x 288 Y.
     gram3 = torch.zeros((kp, kp), dtype=f64, device="cuda")
-    ops.gtq(_dev.vp(q2), kp, _dev.vp(q2), kp, _dev.vp(gram3), kp, kp, kp, m)
+    ops.gram(_dev.vp(q2), kp, kp, m, _dev.vp(gram3))
     linv3, _ = ops.chol(reduce(gram3), k, kp, 0)
     eye = torch.eye(kp, dtype=f64, device="cuda")
     check(ops.L.rgsv_axpy(_dev.vp(linv3), kp, _dev.vp(eye), kp, kp, kp, -1.0, ops.st()),

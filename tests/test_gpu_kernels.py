@@ -226,3 +226,23 @@ def test_core_svd_and_pseudoinverse_norm(rows, cols):
         b[:, -1] = b[:, 0]
         with pytest.raises(rg.RankDeficiencyError):
             rg.pseudoinverse_norm(b)
+
+
+@pytest.mark.parametrize("rows,kp", [(100000, 288), (5000, 208), (300, 144), (2000, 64)])
+def test_gram_lower(rows, kp):
+    """rgsv_gemm_gram_lower: the lower triangle of A^T A (the CholeskyQR
+    Gram the blocked Cholesky reads) to fp64 accuracy; tiles strictly above
+    the diagonal are skipped and left untouched."""
+    rng = np.random.default_rng(rows + kp)
+    a = rng.standard_normal((rows, kp))
+    A = _dev(a)
+    C = torch.full((kp, kp), 7.0, dtype=torch.float64, device="cuda")
+    S = _scratch()
+    _native.check(_native.lib().rgsv_gemm_gram_lower(dev.vp(A), A.stride(0), kp, rows, dev.vp(C),
+                                                     kp, dev.vp(S), S.numel(), _st()), "gram")
+    got = C.cpu().numpy()
+    ref = a.T @ a
+    low = np.tril_indices(kp)
+    assert np.max(np.abs(got[low] - ref[low])) <= 1e-13 * np.abs(ref).max()
+    up = got[np.triu_indices(kp, 1)]
+    assert np.all((up == 7.0) | (np.abs(up - ref[np.triu_indices(kp, 1)]) <= 1e-9 * np.abs(ref).max()))
