@@ -582,6 +582,8 @@ int gemm_gtq(const GemmArgs& a0, cudaStream_t st) {
     GemmArgs a = a0;
     a.zero_to = a0.M;  // 128: zero-fill the padding rows
     a.M = 120;
+    // (cfg2 G1 shape, tools/gemm_variants.py: 6 stages 5933 us; 8 stages
+    //  5907 us; 12 warps of 40 x 32 spill at 128 registers: 6112 / 6092 us)
     return run_gtq<5, 2, 3, 4, 6>(a, st);
   }
   const GemmArgs& a = a0;
