@@ -330,6 +330,14 @@ RGSV_DI void tile_mma_sub(double (&c)[2], const double* Arow8, int lda, const do
   }
 }
 
+// Fragment-major layouts of the panel P (kp x 8) and block row XR (8 x kp):
+// each 8 x 4 DMMA operand fragment is 32 consecutive doubles, so fragment
+// loads are bank-conflict free (the row-major ld-8 / ld-kp layouts were
+// 4-way conflicted). I, K: multiples of 8; (r, c) / (t, n) inside the tile.
+RGSV_DI int p_idx(int I, int r, int c) { return I * 8 + (c >> 2) * 32 + r * 4 + (c & 3); }
+RGSV_DI int x_idx(int K, int t, int n) { return K * 8 + (t >> 2) * 32 + (t & 3) * 8 + n; }
+constexpr int kCholPad = 8;  // A pitch kp + 8: 16-byte C-fragment rows hit distinct chunks
+
 // Blocked right-looking Cholesky + inverse for kp <= 128, 8-wide blocks.
 // Per block column J: thread 0 factors/inverts the 8x8 diagonal block in
 // registers; warps form the panel P = A[J+1:, J] L_JJ^-T and the block row
@@ -338,7 +346,7 @@ RGSV_DI void tile_mma_sub(double (&c)[2], const double* Arow8, int lda, const do
 // W_IK -= P_I XR_K (inverse RHS). Three barriers per 8 columns.
 // Shared layout: A (kp x lda): lower triangle = Schur complement -> L,
 // strict upper = W^T (W -> L^{-1}, strictly lower part); Wd = diag(W).
-__global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gram, int k, int kp,
+__global__ void __launch_bounds__(512) k_chol_blk(const double* __restrict__ gram, int k, int kp,
                                                   int64_t shift_rows, double* __restrict__ linv,
                                                   double* __restrict__ rinv,
                                                   double* __restrict__ r_upper,
@@ -347,7 +355,7 @@ __global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gra
                                                   int* __restrict__ status,
                                                   long long* __restrict__ prof = nullptr) {
   extern __shared__ double sm[];
-  const int ld = kp + 4;
+  const int ld = kp + kCholPad;
 #define PROF_MARK(slot) \
   if (prof && threadIdx.x == 0) prof[(slot)] = clock64();
   double* A = sm;
@@ -437,8 +445,8 @@ __global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gra
 #pragma unroll
         for (int kk = 0; kk < 8; kk += 4)
           dmma(c, A[(I + g) * ld + J + kk + tq], LJ[g * kCholNB + kk + tq]);
-        P[(I + g) * kCholNB + 2 * tq] = c[0];
-        P[(I + g) * kCholNB + 2 * tq + 1] = c[1];
+        P[p_idx(I, g, 2 * tq)] = c[0];
+        P[p_idx(I, g, 2 * tq + 1)] = c[1];
       } else {
         const int K = (task - npanel) * kCholNB;
         // XR_K[r][n] = sum_t LJ[r][t] * W[J+t][K+n]  (W lower part in A^T, diag in Wd)
@@ -448,8 +456,8 @@ __global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gra
           const double w = col < row ? A[col * ld + row] : (col == row ? Wd[row] : 0.0);
           dmma(c, LJ[g * kCholNB + kk + tq], w);
         }
-        XR[g * kp + K + 2 * tq] = c[0];
-        XR[g * kp + K + 2 * tq + 1] = c[1];
+        XR[x_idx(K, g, 2 * tq)] = c[0];
+        XR[x_idx(K, g, 2 * tq + 1)] = c[1];
       }
     }
     __syncthreads();
@@ -463,13 +471,18 @@ __global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gra
         int ii = 0, rem = task;
         while (rem > ii) { rem -= ii + 1; ++ii; }
         const int I = (Jb + 1 + ii) * kCholNB, K = (Jb + 1 + rem) * kCholNB;
-        double c[2];
         const int r0 = I + g, c0 = K + 2 * tq;
-        c[0] = A[r0 * ld + c0];
-        c[1] = A[r0 * ld + c0 + 1];
-        tile_mma_sub(c, P + I * kCholNB, kCholNB, P + K * kCholNB, kCholNB, true);
-        if (I != K || c0 <= r0) A[r0 * ld + c0] = c[0];
-        if (I != K || c0 + 1 <= r0) A[r0 * ld + c0 + 1] = c[1];
+        const double2 cv = *reinterpret_cast<const double2*>(A + r0 * ld + c0);
+        double c[2] = {cv.x, cv.y};
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4)
+          dmma(c, -P[p_idx(I, g, kk + tq)], P[p_idx(K, g, kk + tq)]);
+        if (I != K) {
+          *reinterpret_cast<double2*>(A + r0 * ld + c0) = make_double2(c[0], c[1]);
+        } else {
+          if (c0 <= r0) A[r0 * ld + c0] = c[0];
+          if (c0 + 1 <= r0) A[r0 * ld + c0 + 1] = c[1];
+        }
       } else if (task < ntrail + ninv) {
         const int v = task - ntrail;
         const int I = (Jb + 1 + v / (Jb + 1)) * kCholNB, K = (v % (Jb + 1)) * kCholNB;
@@ -478,21 +491,24 @@ __global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gra
         const int r0 = I + g, n0 = K + 2 * tq;
         c[0] = A[n0 * ld + r0];
         c[1] = A[(n0 + 1) * ld + r0];
-        tile_mma_sub(c, P + I * kCholNB, kCholNB, XR + K, kp, false);
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4)
+          dmma(c, -P[p_idx(I, g, kk + tq)], XR[x_idx(K, kk + tq, g)]);
         A[n0 * ld + r0] = c[0];
         A[(n0 + 1) * ld + r0] = c[1];
       } else {
         // finalize block column J of L for panel block I
         const int I = (Jb + 1 + (task - ntrail - ninv)) * kCholNB;
         for (int e = lane; e < 64; e += 32)
-          A[(I + (e >> 3)) * ld + J + (e & 7)] = P[(I + (e >> 3)) * kCholNB + (e & 7)];
+          A[(I + (e >> 3)) * ld + J + (e & 7)] = P[p_idx(I, e >> 3, e & 7)];
       }
     }
     // finalize block row J of L^{-1}
     for (int e = tid; e < kCholNB * (J + kCholNB); e += nt) {
       const int r = e / (J + kCholNB), c = e % (J + kCholNB), row = J + r;
-      if (c < row) A[c * ld + row] = XR[r * kp + c];
-      else if (c == row) Wd[row] = XR[r * kp + c];
+      const double xv = XR[x_idx(c & ~7, r, c & 7)];
+      if (c < row) A[c * ld + row] = xv;
+      else if (c == row) Wd[row] = xv;
     }
     __syncthreads();
     PROF_MARK(4 + 4 * Jb);
@@ -532,9 +548,11 @@ __global__ void __launch_bounds__(256) k_chol_blk(const double* __restrict__ gra
 int chol_profile(const double* gram, int k, int kp, double* linv, long long* prof,
                  int* status, cudaStream_t st) {
   if (kp > 128) return RGSV_ERR_DIMENSION;
-  const size_t bytes = ((size_t)kp * (kp + 4) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
+  const size_t bytes =
+      ((size_t)kp * (kp + kCholPad) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
   cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(((size_t)128 * 132 + 128 + 2 * 128 * kCholNB + 64) * sizeof(double)));
+                       (int)(((size_t)128 * (128 + kCholPad) + 128 + 2 * 128 * kCholNB + 64) *
+                             sizeof(double)));
   k_chol_blk<<<1, 128, bytes, st>>>(gram, k, kp, 0, linv, nullptr, nullptr, nullptr, nullptr,
                                     status, prof);
   return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
@@ -1058,21 +1076,26 @@ int chol_inv(const double* gram, int k, int kp, int64_t shift_rows, double* linv
     return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
   }
   if (kp <= 128) {
-    const size_t bytes = ((size_t)kp * (kp + 4) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
+    const size_t bytes =
+        ((size_t)kp * (kp + kCholPad) + kp + 2 * (size_t)kp * kCholNB + 64) * sizeof(double);
     static bool attr_blk = false;
     if (!attr_blk) {
       if (cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(((size_t)128 * 132 + 128 + 2 * 128 * kCholNB + 64) *
+                               (int)(((size_t)128 * (128 + kCholPad) + 128 + 2 * 128 * kCholNB + 64) *
                                      sizeof(double))) != cudaSuccess)
         return RGSV_ERR_CUDA;
       attr_blk = true;
     }
+    // 512 threads for kp > 64 (the rank-8 update phase is latency bound:
+    // kp = 128 78 vs 96 us with 256; cfg2 14.67 -> 14.79 pairs/s), 256 below.
     // RGSV_CHOL_THREADS=128 keeps the CTA <= 16K registers so it can co-reside
-    // with a GEMM CTA of the other chain (slower alone: 41 vs 30 us at k = 60)
-    static int threads = [] {
+    // with a GEMM CTA of the other chain (slower alone: 41 vs 30 us at k = 60).
+    static int forced = [] {
       const char* e = getenv("RGSV_CHOL_THREADS");
-      return (e && atoi(e) == 128) ? 128 : 256;
+      const int v = e ? atoi(e) : 0;
+      return (v == 128 || v == 256 || v == 512) ? v : 0;
     }();
+    const int threads = forced ? forced : (kp > 64 ? 512 : 256);
     k_chol_blk<<<1, threads, bytes, st>>>(gram, k, kp, shift_rows, linv, rinv, r_upper, rdiag,
                                       rdiag_acc, status);
     note_launch();
