@@ -15,6 +15,7 @@
 // iterations of SURVEY.md §8(c)): Y = G Omega; Q = cholqr3(Y); q times
 // { Z = G^T Q; Qhat = cholqr3(Z); Y = G Qhat; Q = cholqr3(Y) }; B = Q^T G.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "rgsv_internal.h"
@@ -744,7 +745,14 @@ int batch_chain_plan(int max_rows, int n, int k, int* cs_out, int* yrows_out) {
   const int kp = k <= 16 ? 16 : 32;
   const int np = n <= 64 ? 64 : 128;
   if (k < 1 || k > 32 || n < 1 || n > 128 || k > n) return RGSV_ERR_DIMENSION;
-  for (int cs = 1; cs <= 8; cs *= 2) {
+  // smallest cluster whose CTAs hold the Y slice; RGSV_BATCH_CS raises the
+  // minimum (tuning; cfg3 measured 79.1k / 55.2k pairs/s at 4 / 8)
+  static const int cs_min = [] {
+    const char* e = getenv("RGSV_BATCH_CS");
+    const int v = e ? atoi(e) : 1;
+    return (v == 2 || v == 4 || v == 8) ? v : 1;
+  }();
+  for (int cs = cs_min; cs <= 8; cs *= 2) {
     const int rpc = (max_rows + cs - 1) / cs;
     const int yrows = (rpc + kTR - 1) / kTR * kTR;
     size_t bytes;
