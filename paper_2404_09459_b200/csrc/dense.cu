@@ -789,7 +789,11 @@ int hhqr(const double* b1, int64_t ld1, int m1, const double* b2, int64_t ld2, i
 // ================================================================ Jacobi
 constexpr int kBJ = 16;       // rows per block
 constexpr int kBP = 2 * kBJ;  // rows per block pair
-constexpr int kInnerSweeps = 8;
+// One inner sweep per block-pair visit (more inner sweeps re-rotate pairs the
+// next outer round revisits anyway): 1000 x 1000 Gaussian 104 -> 55 ms, the
+// reference-default adaptive mode at cfg0 23.4 -> 11.4 ms per pair
+// (RGSV_BJ_INNER overrides; profiles/r02_bjacobi_inner_sweeps.log).
+constexpr int kInnerSweeps = 1;
 
 struct BJacJob {
   double* v;  // nv x len (rows are the vectors), rotated in place
@@ -813,7 +817,8 @@ constexpr int kBjPart = 8 * 10 * 64;
 constexpr size_t kBjSmem = (size_t)(kBjPart + 2 * 32 * 33) * 8;
 
 // Process the block pair (ba, bb): returns 1 if it rotated.
-__device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm, int* s_flag) {
+__device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm, int* s_flag,
+                       int inner_sweeps) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* part = sm;
   double* Gm = sm + kBjPart;
@@ -878,7 +883,7 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
   if (!*s_flag) return 0;
   // ---- cyclic two-sided Jacobi on the Gram, rotations accumulated in R
   const int pr = tid >> 4, sub = tid & 15;
-  for (int isw = 0; isw < kInnerSweeps; ++isw) {
+  for (int isw = 0; isw < inner_sweeps; ++isw) {
     __syncthreads();
     if (tid == 0) *s_flag = 0;
     __syncthreads();
@@ -969,7 +974,8 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
 }
 
 __global__ void __launch_bounds__(kDenseThreads) k_bjacobi(BJacJob j0, BJacJob j1, int max_sweeps,
-                                                           int* __restrict__ status) {
+                                                           int* __restrict__ status,
+                                                           int inner_sweeps) {
   extern __shared__ double dsm[];
   __shared__ int s_flag;
   const BJacJob J = (int)blockIdx.x < j0.cta0 + j0.ctas ? j0 : j1;
@@ -992,7 +998,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_bjacobi(BJacJob j0, BJacJob j
       for (int p = cta; p < npairs; p += J.ctas) {
         // (one block: nbe = 2 and its partner block is all padding)
         const int ba = rr_player(p, round, nbe), bb = rr_player(nbe - 1 - p, round, nbe);
-        rotated |= bj_pair(J, ba, bb, tol, dsm, &s_flag);
+        rotated |= bj_pair(J, ba, bb, tol, dsm, &s_flag, inner_sweeps);
       }
       if (J.ctas > 1) grid_barrier(J.bar, J.ctas, epoch);
     }
@@ -1064,7 +1070,13 @@ int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, 
   BJacJob b{v2, ld2, nv2, len2, sv2, nsv2, reinterpret_cast<unsigned*>(s + 64 + kBjMaxSweeps * 4),
             reinterpret_cast<int*>(s + 128 + kBjMaxSweeps * 4), c1, c2};
   int ms = kBjMaxSweeps;
-  void* args[] = {&a, &b, &ms, &status};
+  static const int inner = [] {  // RGSV_BJ_INNER: inner Jacobi sweeps per block pair
+    const char* e = getenv("RGSV_BJ_INNER");
+    const int v = e ? atoi(e) : kInnerSweeps;
+    return v >= 1 && v <= 16 ? v : kInnerSweeps;
+  }();
+  int isw = inner;
+  void* args[] = {&a, &b, &ms, &status, &isw};
   return coop_launch(reinterpret_cast<const void*>(k_bjacobi), c1 + c2, kDenseThreads, smem,
                      args, st);
 }
