@@ -52,6 +52,14 @@ RGSV_DI void grid_barrier(unsigned* ctr, unsigned nblocks, unsigned& epoch) {
   __syncthreads();
 }
 
+// Hardware barrier over the CTAs of this thread-block cluster (all threads).
+RGSV_DI void cluster_sync_all() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::
+          : "memory");
+}
+
 RGSV_DI double block_sum(double v, double* red) {  // blockDim.x = 256, red >= 8 doubles
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_sum(v);
@@ -683,20 +691,10 @@ size_t hhqr_workspace_bytes(int M, int N) {
   return (size_t)M * lda * 8 + npan * 32 * 33 * 8 + 1024;
 }
 
-// Grid-barrier kernels launch cooperatively (all CTAs co-resident) when the
-// grid is large. Small grids (<= kPlainGrid CTAs, one per SM) launch plainly:
-// a cooperative launch holds back concurrent work on other streams (cfg1
-// with 8 concurrent pairs: 694 vs 736 pairs/s), and a few CTAs always become
-// resident as the (finite) kernels of the other streams retire, so the
-// barrier cannot deadlock. RGSV_COOP_ALL=1 forces cooperative launches.
-constexpr int kPlainGrid = 32;
-
+// Grid-barrier kernels launch cooperatively: all CTAs co-resident, so the
+// global-memory barrier cannot wait on a CTA that is not scheduled.
 static int coop_launch(const void* fn, int grid, int threads, size_t smem, void** args,
                        cudaStream_t st) {
-  static const bool coop_all = [] {
-    const char* e = getenv("RGSV_COOP_ALL");
-    return e && atoi(e) != 0;
-  }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -706,7 +704,7 @@ static int coop_launch(const void* fn, int grid, int threads, size_t smem, void*
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (coop_all || grid > kPlainGrid) ? 1 : 0;
+  cfg.numAttrs = 1;
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return RGSV_ERR_CUDA;
   note_launch();
   return 0;
@@ -806,6 +804,7 @@ struct BJacJob {
   int* flags;     // zeroed, max_sweeps entries: a rotation happened in sweep s
   int cta0;       // first CTA of this job
   int ctas;       // CTAs of this job
+  int cluster;    // 1: the job is one thread-block cluster (hardware barrier)
 };
 
 RGSV_DI int rr_player(int p, int round, int nplayers) {
@@ -1000,10 +999,14 @@ __global__ void __launch_bounds__(kDenseThreads) k_bjacobi(BJacJob j0, BJacJob j
         const int ba = rr_player(p, round, nbe), bb = rr_player(nbe - 1 - p, round, nbe);
         rotated |= bj_pair(J, ba, bb, tol, dsm, &s_flag, inner_sweeps);
       }
-      if (J.ctas > 1) grid_barrier(J.bar, J.ctas, epoch);
+      if (J.ctas > 1) {
+        if (J.cluster) cluster_sync_all();
+        else grid_barrier(J.bar, J.ctas, epoch);
+      }
     }
     if (rotated && tid == 0) atomicOr(J.flags + sweep, 1);
-    if (J.ctas > 1) grid_barrier(J.bar, J.ctas, epoch);
+    if (J.ctas > 1 && J.cluster) cluster_sync_all();
+    else if (J.ctas > 1) grid_barrier(J.bar, J.ctas, epoch);
     else __syncthreads();
     converged = ld_acquire_u32(reinterpret_cast<unsigned*>(J.flags + sweep)) == 0;
     __syncthreads();
@@ -1065,10 +1068,19 @@ int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, 
   const int cap = c2 > 0 ? kSMs / 2 : kSMs;
   if (c1 > cap) c1 = cap;
   if (c2 > cap) c2 = cap;
+  // small jobs: one thread-block cluster per job (gang-scheduled, hardware
+  // cluster barrier), both jobs padded to the same CTA count; larger jobs: one
+  // cooperative launch with global-memory barriers
+  const int cmax = c1 > c2 ? c1 : c2;
+  const bool clustered = cmax <= 8;
+  if (clustered) {
+    c1 = cmax;
+    if (c2 > 0) c2 = cmax;
+  }
   BJacJob a{v1, ld1, nv1, len1, sv1, nsv1, reinterpret_cast<unsigned*>(s),
-            reinterpret_cast<int*>(s + 64), 0, c1};
+            reinterpret_cast<int*>(s + 64), 0, c1, clustered ? 1 : 0};
   BJacJob b{v2, ld2, nv2, len2, sv2, nsv2, reinterpret_cast<unsigned*>(s + 64 + kBjMaxSweeps * 4),
-            reinterpret_cast<int*>(s + 128 + kBjMaxSweeps * 4), c1, c2};
+            reinterpret_cast<int*>(s + 128 + kBjMaxSweeps * 4), c1, c2, clustered ? 1 : 0};
   int ms = kBjMaxSweeps;
   static const int inner = [] {  // RGSV_BJ_INNER: inner Jacobi sweeps per block pair
     const char* e = getenv("RGSV_BJ_INNER");
@@ -1077,8 +1089,25 @@ int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, 
   }();
   int isw = inner;
   void* args[] = {&a, &b, &ms, &status, &isw};
-  return coop_launch(reinterpret_cast<const void*>(k_bjacobi), c1 + c2, kDenseThreads, smem,
-                     args, st);
+  if (!clustered)
+    return coop_launch(reinterpret_cast<const void*>(k_bjacobi), c1 + c2, kDenseThreads, smem,
+                       args, st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c1 + c2);
+  cfg.blockDim = dim3(kDenseThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute cl[1];
+  cl[0].id = cudaLaunchAttributeClusterDimension;
+  cl[0].val.clusterDim.x = c1;
+  cl[0].val.clusterDim.y = 1;
+  cl[0].val.clusterDim.z = 1;
+  cfg.attrs = cl;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_bjacobi), args) != cudaSuccess)
+    return RGSV_ERR_CUDA;
+  note_launch();
+  return 0;
 }
 
 }  // namespace rgsv
