@@ -133,6 +133,14 @@ int rgsv_orth_complete(double* a, int64_t lda, int dim, int have, int count, dou
 int rgsv_svd_vectors(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
                      double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj, int ascending,
                      int* nzero, int* status, void* stream);
+/* rgsv_svd_vectors on many CTAs (blocked one-sided Jacobi with the 32 x 32
+ * block rotations accumulated into acc; nv <= len, nv up to 25600): same
+ * outputs. workspace >= rgsv_svd_vectors_blocked_workspace_bytes(nv). */
+size_t rgsv_svd_vectors_blocked_workspace_bytes(int nv);
+int rgsv_svd_vectors_blocked(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                             double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj,
+                             int ascending, int* nzero, int* status, void* workspace,
+                             size_t workspace_bytes, void* stream);
 /* dst (cols x rows) = src^T, src rows x cols. */
 int rgsv_transpose(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
                    void* stream);

@@ -49,6 +49,9 @@ SIGNATURES = {
     "rgsv_householder_qr": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _p]),
     "rgsv_axpy": (_i32, [_p, _i64, _p, _i64, _i32, _i32, _d, _p]),
     "rgsv_orth_complete": (_i32, [_p, _i64, _i32, _i32, _i32, _p, _i64, _p, _p, _p]),
+    "rgsv_svd_vectors_blocked_workspace_bytes": (_sz, [_i32]),
+    "rgsv_svd_vectors_blocked": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _i64, _p, _i64,
+                                        _i32, _p, _p, _p, _sz, _p]),
     "rgsv_svd_vectors": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _i64, _p, _i64, _i32,
                                 _p, _p, _p]),
     "rgsv_transpose": (_i32, [_p, _i64, _p, _i64, _i32, _i32, _p]),

@@ -225,6 +225,19 @@ int rgsv_svd_vectors(double* v, int64_t ldv, int nv, int len, double* acc, int64
                            status, reinterpret_cast<cudaStream_t>(stream));
 }
 
+size_t rgsv_svd_vectors_blocked_workspace_bytes(int nv) {
+  return svd_vectors_blocked_workspace_bytes(nv);
+}
+
+int rgsv_svd_vectors_blocked(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                             double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj,
+                             int ascending, int* nzero, int* status, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  return svd_vectors_blocked(v, ldv, nv, len, acc, ldacc, sv, xn, ldx, jo, ldj, ascending, nzero,
+                             status, workspace, workspace_bytes,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
 int rgsv_transpose(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols,
                    void* stream) {
   if (rows < 0 || cols < 0 || ldd < rows || lds < cols) return RGSV_ERR_DIMENSION;

@@ -805,6 +805,8 @@ struct BJacJob {
   int cta0;       // first CTA of this job
   int ctas;       // CTAs of this job
   int cluster;    // 1: the job is one thread-block cluster (hardware barrier)
+  double* acc;    // optional nv x nv accumulated rotations (starts at I), ld ldacc
+  int64_t ldacc;
 };
 
 RGSV_DI int rr_player(int p, int round, int nplayers) {
@@ -951,13 +953,19 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
     for (int e = tid; e < 1024; e += kDenseThreads) R[(e >> 5) * 33 + (e & 31)] = Rn[e];
     __syncthreads();
   }
-  // ---- rotate the pair's rows: Vp <- R Vp
-  for (int k = tid; k < J.len; k += kDenseThreads) {
+  // ---- rotate the pair's rows: Vp <- R Vp (and the same rows of the
+  //      accumulated rotations when singular vectors are requested)
+  const int ncols = J.acc ? J.len + J.nv : J.len;
+  for (int kk = tid; kk < ncols; kk += kDenseThreads) {
+    const bool in_acc = kk >= J.len;
+    double* base = in_acc ? J.acc : J.v;
+    const int64_t ld = in_acc ? J.ldacc : J.ld;
+    const int k = in_acc ? kk - J.len : kk;
     double x[kBP];
 #pragma unroll
     for (int i = 0; i < kBP; ++i) {
       const int gr = i < kBJ ? ba * kBJ + i : bb * kBJ + (i - kBJ);
-      x[i] = gr < J.nv ? J.v[(int64_t)gr * J.ld + k] : 0.0;
+      x[i] = gr < J.nv ? base[(int64_t)gr * ld + k] : 0.0;
     }
 #pragma unroll 4
     for (int i = 0; i < kBP; ++i) {
@@ -965,7 +973,7 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
       double y = 0.0;
 #pragma unroll
       for (int j = 0; j < kBP; ++j) y = fma(R[i * 33 + j], x[j], y);
-      if (gr < J.nv) J.v[(int64_t)gr * J.ld + k] = y;
+      if (gr < J.nv) base[(int64_t)gr * ld + k] = y;
     }
   }
   __syncthreads();
@@ -989,6 +997,16 @@ __global__ void __launch_bounds__(kDenseThreads) k_bjacobi(BJacJob j0, BJacJob j
   const int nbe = nblk + (nblk & 1);
   const int npairs = nbe / 2;
   unsigned epoch = 0;
+  if (J.acc) {  // accumulated rotations start at the identity
+    for (int64_t e = (int64_t)cta * kDenseThreads + tid; e < (int64_t)J.nv * J.nv;
+         e += (int64_t)J.ctas * kDenseThreads) {
+      const int i = (int)(e / J.nv), j = (int)(e % J.nv);
+      J.acc[(int64_t)i * J.ldacc + j] = (i == j) ? 1.0 : 0.0;
+    }
+    if (J.ctas > 1 && J.cluster) cluster_sync_all();
+    else if (J.ctas > 1) grid_barrier(J.bar, J.ctas, epoch);
+    else __syncthreads();
+  }
   bool converged = nblk == 1 && J.nv == 1;
   int sweep = 0;
   for (; sweep < max_sweeps && !converged; ++sweep) {
@@ -1042,9 +1060,20 @@ size_t bjacobi_sync_bytes() { return 2 * (64 + kBjMaxSweeps * 4) + 256; }
 
 // Singular values of the rows of two matrices (either may be empty) by
 // blocked one-sided Jacobi; `sync` >= bjacobi_sync_bytes() of scratch.
+int bjacobi_acc(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, double* acc1,
+                int64_t ldacc1, double* v2, int64_t ld2, int nv2, int len2, double* sv2,
+                int* nsv2, int* status, void* sync, cudaStream_t st);
+
 int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, double* v2,
             int64_t ld2, int nv2, int len2, double* sv2, int* nsv2, int* status, void* sync,
             cudaStream_t st) {
+  return bjacobi_acc(v1, ld1, nv1, len1, sv1, nsv1, nullptr, 0, v2, ld2, nv2, len2, sv2, nsv2,
+                     status, sync, st);
+}
+
+int bjacobi_acc(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, double* acc1,
+                int64_t ldacc1, double* v2, int64_t ld2, int nv2, int len2, double* sv2,
+                int* nsv2, int* status, void* sync, cudaStream_t st) {
   if (nv1 < 0 || nv2 < 0) return RGSV_ERR_DIMENSION;
   const size_t smem_n = (size_t)(nv1 > nv2 ? nv1 : nv2) * 8;
   if (smem_n > 200 * 1024) return RGSV_ERR_DIMENSION;  // nv <= 25600
@@ -1078,9 +1107,10 @@ int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, 
     if (c2 > 0) c2 = cmax;
   }
   BJacJob a{v1, ld1, nv1, len1, sv1, nsv1, reinterpret_cast<unsigned*>(s),
-            reinterpret_cast<int*>(s + 64), 0, c1, clustered ? 1 : 0};
+            reinterpret_cast<int*>(s + 64), 0, c1, clustered ? 1 : 0, acc1, ldacc1};
   BJacJob b{v2, ld2, nv2, len2, sv2, nsv2, reinterpret_cast<unsigned*>(s + 64 + kBjMaxSweeps * 4),
-            reinterpret_cast<int*>(s + 128 + kBjMaxSweeps * 4), c1, c2, clustered ? 1 : 0};
+            reinterpret_cast<int*>(s + 128 + kBjMaxSweeps * 4), c1, c2, clustered ? 1 : 0,
+            nullptr, 0};
   int ms = kBjMaxSweeps;
   static const int inner = [] {  // RGSV_BJ_INNER: inner Jacobi sweeps per block pair
     const char* e = getenv("RGSV_BJ_INNER");
@@ -1108,6 +1138,82 @@ int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, 
     return RGSV_ERR_CUDA;
   note_launch();
   return 0;
+}
+
+// ---------------------------------------- singular vectors from the rotated rows
+// After k_bjacobi with an accumulator: v rows = diag(s) X rows (orthogonal),
+// acc = J (orthogonal), J A = v. Outputs ordered by singular value
+// (descending, or ascending): sv, xn = unit rows of X (zero rows stay zero and
+// are counted in *nzero), jo = the matching rows of J -- the contract of
+// k_jacobi_vec (small.cu), on many CTAs.
+__global__ void k_vec_norms(const double* __restrict__ v, int64_t ldv, int nv, int len,
+                            double* __restrict__ nrm) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= nv) return;
+  const double* vi = v + (int64_t)row * ldv;
+  double s = 0.0;
+  for (int e = lane; e < len; e += 32) s = fma(vi[e], vi[e], s);
+  s = warp_sum(s);
+  if (lane == 0) nrm[row] = sqrt(s);
+}
+
+__global__ void k_vec_rank(const double* __restrict__ nrm, int nv, int ascending,
+                           int* __restrict__ ord, double* __restrict__ sv,
+                           int* __restrict__ nzero) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const double x = nrm[i];
+  int rank = 0;
+  for (int j = 0; j < nv; ++j) {
+    const double y = nrm[j];
+    rank += ascending ? ((y < x) || (y == x && j < i)) : ((y > x) || (y == x && j < i));
+  }
+  ord[rank] = i;
+  sv[rank] = x;
+  if (x == 0.0) atomicAdd(nzero, 1);
+}
+
+__global__ void k_vec_gather(const double* __restrict__ v, int64_t ldv, const double* __restrict__ acc,
+                             int64_t ldacc, int nv, int len, const double* __restrict__ nrm,
+                             const int* __restrict__ ord, double* __restrict__ xn, int64_t ldx,
+                             double* __restrict__ jo, int64_t ldj) {
+  const int lane = threadIdx.x & 31;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= nv) return;
+  const int i = ord[r];
+  const double x = nrm[i];
+  const double inv = x > 0.0 ? 1.0 / x : 0.0;
+  for (int e = lane; e < len; e += 32) xn[(int64_t)r * ldx + e] = v[(int64_t)i * ldv + e] * inv;
+  for (int e = lane; e < nv; e += 32) jo[(int64_t)r * ldj + e] = acc[(int64_t)i * ldacc + e];
+}
+
+size_t svd_vectors_blocked_workspace_bytes(int nv) {
+  return bjacobi_sync_bytes() + (size_t)nv * 16 + 512;
+}
+
+int svd_vectors_blocked(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                        double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj,
+                        int ascending, int* nzero, int* status, void* ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  if (nv < 1 || len < 1 || nv > len) return RGSV_ERR_DIMENSION;
+  if (ws_bytes < svd_vectors_blocked_workspace_bytes(nv)) return RGSV_ERR_WORKSPACE;
+  char* w = static_cast<char*>(ws);
+  void* sync = w;
+  double* nrm = reinterpret_cast<double*>(w + ((bjacobi_sync_bytes() + 255) & ~size_t(255)));
+  int* ord = reinterpret_cast<int*>(nrm + nv);
+  double* sv_tmp = sv;  // k_bjacobi's own descending values, overwritten below
+  int* nsv_tmp = ord;   // scratch for its count (ord is written after)
+  if (int e = bjacobi_acc(v, ldv, nv, len, sv_tmp, nsv_tmp, acc, ldacc, nullptr, 0, 0, len,
+                          nullptr, nullptr, status, sync, st))
+    return e;
+  if (cudaMemsetAsync(nzero, 0, sizeof(int), st) != cudaSuccess) return RGSV_ERR_CUDA;
+  const int wblocks = (nv * 32 + 255) / 256;
+  k_vec_norms<<<wblocks, 256, 0, st>>>(v, ldv, nv, len, nrm);
+  k_vec_rank<<<(nv + 255) / 256, 256, 0, st>>>(nrm, nv, ascending, ord, sv, nzero);
+  k_vec_gather<<<wblocks, 256, 0, st>>>(v, ldv, acc, ldacc, nv, len, nrm, ord, xn, ldx, jo, ldj);
+  note_launch(3);
+  return cudaGetLastError() == cudaSuccess ? 0 : RGSV_ERR_CUDA;
 }
 
 }  // namespace rgsv

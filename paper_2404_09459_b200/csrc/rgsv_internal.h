@@ -119,5 +119,12 @@ size_t bjacobi_sync_bytes();
 int bjacobi(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* nsv1, double* v2,
             int64_t ld2, int nv2, int len2, double* sv2, int* nsv2, int* status, void* sync,
             cudaStream_t st);
+// Singular values AND vectors of the rows of v (nv <= len) by the blocked
+// Jacobi with accumulated rotations; the k_jacobi_vec output contract.
+size_t svd_vectors_blocked_workspace_bytes(int nv);
+int svd_vectors_blocked(double* v, int64_t ldv, int nv, int len, double* acc, int64_t ldacc,
+                        double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj,
+                        int ascending, int* nzero, int* status, void* ws, size_t ws_bytes,
+                        cudaStream_t st);
 
 }  // namespace rgsv

@@ -15,8 +15,9 @@ C1 = Q1ᵀG1, C2 = Q2ᵀG2 (or G1, G2 themselves for method="direct"):
 
 All arithmetic runs in librgsv_b200.so; torch only allocates, slices and
 flips buffers. Meaningful in the adaptive / direct regime, where
-l1 + l2 >= n; the stacked width n is limited to 1024
-(the blocked Cholesky and the one-CTA Householder / Jacobi kernels).
+l1 + l2 >= n; the stacked width n is limited to 4096
+(the blocked Cholesky; SVDs with vectors of 64+ vectors run on the blocked
+multi-CTA Jacobi, completions beyond 1024 columns by projected CholeskyQR3).
 """
 
 from __future__ import annotations
@@ -27,7 +28,7 @@ import numpy as np
 import torch
 
 from . import device as _dev
-from ._native import ST_JACOBI, check
+from ._native import ST_CHOL, ST_JACOBI, check
 from .errors import ConvergenceError, RecoveryError
 from .rangefinder import _block_qr, _Ops, adaptive_device
 
@@ -76,13 +77,19 @@ class _Dense:
     def complete(self, cols, dim: int, have: int, count: int) -> torch.Tensor:
         """`count` orthonormal columns orthogonal to cols[:, :have]
         (engine.py:278-291): np.eye(dim, count) when have == 0, else columns
-        have..have+count of the complete Householder Q."""
+        have..have+count of the complete Householder Q (one-CTA kernel, up to
+        1024 columns each side), or beyond that a Gaussian block projected off
+        cols twice and orthonormalized by shifted CholeskyQR3. Completion
+        columns multiply classified-zero GSVs and are not determined by the
+        data: any orthonormal completion is the reference's contract."""
         if have + count > dim:
             raise RecoveryError(f"cannot complete {have} columns with {count} more in "
                                 f"dimension {dim}")
         out = _buf(dim, count)
         if count == 0:
             return out
+        if have > 1024 or count > 1024:
+            return self._complete_projected(cols, dim, have, count)
         a = _buf(dim, max(have, 1))
         if have:
             a[:dim, :have] = cols[:dim, :have]
@@ -91,6 +98,26 @@ class _Dense:
         check(self.L.rgsv_orth_complete(_dev.vp(a), a.stride(0), dim, have, count, _dev.vp(out),
                                         out.stride(0), _dev.vp(rd), _dev.vp(tau), self.st()),
               "orth_complete")
+        return out
+
+    def _complete_projected(self, cols, dim: int, have: int, count: int) -> torch.Tensor:
+        kp = _dev.ceil16(count)
+        om = _dev.omega_device(dim, count, [0x5EED + have])[0]   # count x ldo (device)
+        x = self.tr(om, count, dim)                              # dim x count
+        x = x[:dim]
+        for _ in range(2):                                       # x -= C (C^T x), twice
+            t = self.at_b(cols, dim, have, x, count)             # have x count
+            proj = self.mm_bt(cols, dim, have, self.tr(t, have, count), count)
+            check(self.L.rgsv_axpy(_dev.vp(x), x.stride(0), _dev.vp(proj), proj.stride(0), dim,
+                                   count, -1.0, self.st()), "axpy")
+        y = torch.zeros((dim, kp), dtype=F64, device="cuda")
+        y[:, :count] = x[:, :count]
+        self.ops.status.zero_()
+        q = self.ops.cholqr3(y, dim, count, kp)
+        if int(self.ops.status.item()) & ST_CHOL:
+            raise RecoveryError("orthonormal completion failed (CholeskyQR breakdown)")
+        out = _buf(dim, count)
+        out[:dim, :count] = q[:, :count]
         return out
 
     def scale_cols(self, a, rows: int, cols: int, d: torch.Tensor):
@@ -115,10 +142,18 @@ class _Dense:
         jo = _buf(nv, nv)
         xn = _buf(nv, ln)
         sv = torch.zeros(nv, dtype=F64, device="cuda")
-        check(self.L.rgsv_svd_vectors(_dev.vp(v), v.stride(0), nv, ln, _dev.vp(acc),
-                                      acc.stride(0), _dev.vp(sv), _dev.vp(xn), xn.stride(0),
-                                      _dev.vp(jo), jo.stride(0), 0, _dev.vp(status[1:2]),
-                                      _dev.vp(status[0:1]), self.st()), "svd_vectors")
+        if nv >= 64:  # blocked multi-CTA Jacobi with accumulated rotations
+            nb = int(self.L.rgsv_svd_vectors_blocked_workspace_bytes(nv))
+            ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            check(self.L.rgsv_svd_vectors_blocked(
+                _dev.vp(v), v.stride(0), nv, ln, _dev.vp(acc), acc.stride(0), _dev.vp(sv),
+                _dev.vp(xn), xn.stride(0), _dev.vp(jo), jo.stride(0), 0, _dev.vp(status[1:2]),
+                _dev.vp(status[0:1]), _dev.vp(ws), nb, self.st()), "svd_vectors_blocked")
+        else:
+            check(self.L.rgsv_svd_vectors(_dev.vp(v), v.stride(0), nv, ln, _dev.vp(acc),
+                                          acc.stride(0), _dev.vp(sv), _dev.vp(xn), xn.stride(0),
+                                          _dev.vp(jo), jo.stride(0), 0, _dev.vp(status[1:2]),
+                                          _dev.vp(status[0:1]), self.st()), "svd_vectors")
         code, nzero = (int(x) for x in status[:2].cpu().tolist())
         if code & ST_JACOBI:
             raise ConvergenceError("Jacobi SVD of an L block did not converge")
@@ -173,8 +208,8 @@ def recover(pair, opts, direct: bool):
     if min(l, n) != n:                                   # engine.py:309-313
         raise RecoveryError("compressed pair has fewer than n independent columns; "
                             "tighten the extraction tolerance")
-    if n > 1024:
-        raise RecoveryError(f"device recovery supports n <= 1024, got n={n}")
+    if n > 4096:
+        raise RecoveryError(f"device recovery supports n <= 4096, got n={n}")
     spec: GsvSpectrum = _spectrum_checked(c1, l1, c2, l2, n, opts.classify_tol)
     alphas, betas, r, s = spec.alphas, spec.betas, spec.r, spec.s
     tol = opts.classify_tol

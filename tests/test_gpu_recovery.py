@@ -224,3 +224,33 @@ def test_recovery_cfg0_adaptive_matches_reference(rg):
                                                                        seed=0)))
     worst = _compare(fac, gold, "cfg0_adaptive", 3e-5, 1e-7)
     print("cfg0 adaptive worst principal angle vs reference:", worst)
+
+
+# ------------------------------------------------------------ n > 1024
+def test_recovery_beyond_1024_columns_direct(rg):
+    """n = 1100 (round 1 stopped at 1024): blocked Jacobi with vectors for the
+    L-block SVD; the reference's invariants (test_engine.py:177-186) and the
+    oracle's direct-method spectrum."""
+    m, p, n = 1300, 1250, 1100
+    g1, g2 = orc.gaussian_matrix(m, n, 31), orc.gaussian_matrix(p, n, 32)
+    pair = rg.GmpPair(g1, g2)
+    fac = rg.recover_gsvd(pair, rg.GsvOptions(method="direct"))
+    _check_factors(pair, fac, g1, g2)
+    o = orc.run_pipeline(g1, g2, direct=True)
+    assert (fac.spectrum.r, fac.spectrum.s) == (o.r, o.s)
+    assert np.max(np.abs(fac.spectrum.alphas - o.alphas)) <= 1e-10
+
+
+def test_recovery_wide_completion_beyond_1024(rg):
+    """r = 1060 classified zeros of beta at n = 1100: the V completion needs
+    1060 columns (projected Gaussian + shifted CholeskyQR3 path)."""
+    n = 1100
+    alphas = np.concatenate([np.ones(1060), np.linspace(0.9, 0.1, 40)])
+    pair = _structured_pair(rg, alphas, 1200, 1150, 41)
+    fac = rg.recover_gsvd(pair, rg.GsvOptions(method="direct"))
+    assert fac.spectrum.r == 1060
+    g1, g2 = pair.g1.t.cpu().numpy(), pair.g2.t.cpu().numpy()
+    _check_factors(pair, fac, g1, g2)
+    vz = fac.v[:, :1060]
+    assert np.linalg.norm(vz.T @ fac.v[:, 1060:]) <= 1e-10
+    assert np.linalg.norm(vz.T @ vz - np.eye(1060)) <= 1e-10 * np.sqrt(1060)
