@@ -229,8 +229,8 @@ def svd(m) -> SvdFactors:
 
     g = as_matrix(m)
     rows, cols = g.rows, g.cols
-    if min(rows, cols) > 2048:
-        raise DimensionError("B200 svd supports min(rows, cols) <= 2048 (one-sided Jacobi)")
+    if min(rows, cols) > 8192:
+        raise DimensionError("B200 svd supports min(rows, cols) <= 8192 (blocked Jacobi)")
     blk = _buf(rows, cols)
     blk[:rows, :cols] = g.t
     dense = _Dense()

@@ -96,3 +96,19 @@ def test_rank_check_beyond_limit_is_explicit():
     pair = rg.GmpPair(g, g.clone(), check_rank=False)
     with pytest.raises(rg.DimensionError):
         _ = pair.stack_norm2
+
+
+@pytest.mark.parametrize("rows,cols", [(2100, 2200), (2300, 150)])
+def test_svd_with_vectors_blocked(rows, cols):
+    """core.svd (core.py:99-106) beyond the one-CTA Jacobi's 2048 vectors:
+    blocked Jacobi with accumulated rotations; values vs LAPACK,
+    reconstruction and orthonormal factors."""
+    rng = np.random.default_rng(rows)
+    a = rng.standard_normal((rows, cols))
+    f = rg.svd(a)
+    ref = np.linalg.svd(a, compute_uv=False)
+    k = min(rows, cols)
+    assert np.max(np.abs(f.s - ref)) <= 1e-12 * ref[0]
+    assert np.linalg.norm((f.u * f.s) @ f.v.T - a) <= 1e-12 * np.linalg.norm(a)
+    assert np.linalg.norm(f.u.T @ f.u - np.eye(k)) <= 1e-11 * np.sqrt(k)
+    assert np.linalg.norm(f.v.T @ f.v - np.eye(k)) <= 1e-11 * np.sqrt(k)
