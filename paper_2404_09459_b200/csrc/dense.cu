@@ -891,12 +891,13 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
     for (int round = 0; round < 31; ++round) {
       const int a = rr_player(pr, round, 32), b = rr_player(31 - pr, round, 32);
       const double al = Gm[a * 33 + a], be = Gm[b * 33 + b], ga = Gm[a * 33 + b];
-      const bool rot = ga != 0.0 && fabs(ga) > tol * sqrt(al * be);
+      // |ga| > tol sqrt(al be), squared (al, be >= 0): no sqrt on the chain
+      const bool rot = ga != 0.0 && ga * ga > (tol * tol) * (al * be);
       double c = 1.0, s = 0.0, tt = 0.0;
       if (rot) {
         const double zeta = (be - al) / (2.0 * ga);
-        tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        c = 1.0 / sqrt(1.0 + tt * tt);
+        tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        c = rsqrt(fma(tt, tt, 1.0));
         s = c * tt;
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -911,21 +912,24 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
       }
       __syncthreads();
       if (rot) {
+        // column update; the pair's own 2 x 2 block gets its exact values
+        // here (no third barrier): diag al - t ga, be + t ga, off-diagonal 0
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
           const int row = sub + 16 * h2;
-          const double x = Gm[row * 33 + a], y = Gm[row * 33 + b];
-          Gm[row * 33 + a] = c * x - s * y;
-          Gm[row * 33 + b] = s * x + c * y;
+          if (row == a) {
+            Gm[a * 33 + a] = al - tt * ga;
+            Gm[a * 33 + b] = 0.0;
+          } else if (row == b) {
+            Gm[b * 33 + a] = 0.0;
+            Gm[b * 33 + b] = be + tt * ga;
+          } else {
+            const double x = Gm[row * 33 + a], y = Gm[row * 33 + b];
+            Gm[row * 33 + a] = c * x - s * y;
+            Gm[row * 33 + b] = s * x + c * y;
+          }
         }
-      }
-      __syncthreads();
-      if (rot && sub == 0) {
-        Gm[a * 33 + a] = al - tt * ga;
-        Gm[b * 33 + b] = be + tt * ga;
-        Gm[a * 33 + b] = 0.0;
-        Gm[b * 33 + a] = 0.0;
-        *s_flag = 1;
+        if (sub == 0) *s_flag = 1;
       }
       __syncthreads();
     }
@@ -954,26 +958,48 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
     __syncthreads();
   }
   // ---- rotate the pair's rows: Vp <- R Vp (and the same rows of the
-  //      accumulated rotations when singular vectors are requested)
-  const int ncols = J.acc ? J.len + J.nv : J.len;
-  for (int kk = tid; kk < ncols; kk += kDenseThreads) {
-    const bool in_acc = kk >= J.len;
-    double* base = in_acc ? J.acc : J.v;
-    const int64_t ld = in_acc ? J.ldacc : J.ld;
-    const int k = in_acc ? kk - J.len : kk;
-    double x[kBP];
+  //      accumulated rotations when singular vectors are requested), on
+  //      DMMA: R's fragments in registers, 8-column blocks of the 32 rows per
+  //      warp iteration (loads of a block complete before its stores)
+  {
+    const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    double rf[4][8];  // A fragments: R[mt*8 + g][ks*4 + t]
 #pragma unroll
-    for (int i = 0; i < kBP; ++i) {
-      const int gr = i < kBJ ? ba * kBJ + i : bb * kBJ + (i - kBJ);
-      x[i] = gr < J.nv ? base[(int64_t)gr * ld + k] : 0.0;
-    }
-#pragma unroll 4
-    for (int i = 0; i < kBP; ++i) {
-      const int gr = i < kBJ ? ba * kBJ + i : bb * kBJ + (i - kBJ);
-      double y = 0.0;
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int j = 0; j < kBP; ++j) y = fma(R[i * 33 + j], x[j], y);
-      if (gr < J.nv) base[(int64_t)gr * ld + k] = y;
+      for (int ks = 0; ks < 8; ++ks) rf[mt][ks] = R[(mt * 8 + g) * 33 + ks * 4 + t];
+    const int nb_v = (J.len + 7) / 8;
+    const int nb_all = J.acc ? nb_v + (J.nv + 7) / 8 : nb_v;
+    for (int blk = warp; blk < nb_all; blk += kDenseThreads / 32) {
+      const bool in_acc = blk >= nb_v;
+      double* base = in_acc ? J.acc : J.v;
+      const int64_t ld = in_acc ? J.ldacc : J.ld;
+      const int ncol = in_acc ? J.nv : J.len;
+      const int n0 = (in_acc ? blk - nb_v : blk) * 8;
+      double bf[8];  // B fragments: Vp[ks*4 + t][n0 + g]
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int i = ks * 4 + t;
+        const int gr = i < kBJ ? ba * kBJ + i : bb * kBJ + (i - kBJ);
+        bf[ks] = (gr < J.nv && n0 + g < ncol) ? base[(int64_t)gr * ld + n0 + g] : 0.0;
+      }
+      double cacc[4][2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) cacc[mt][0] = cacc[mt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) dmma(cacc[mt], rf[mt][ks], bf[ks]);
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int i = mt * 8 + g;
+        const int gr = i < kBJ ? ba * kBJ + i : bb * kBJ + (i - kBJ);
+        if (gr >= J.nv) continue;
+        const int col = n0 + 2 * t;
+        if (col < ncol) base[(int64_t)gr * ld + col] = cacc[mt][0];
+        if (col + 1 < ncol) base[(int64_t)gr * ld + col + 1] = cacc[mt][1];
+      }
     }
   }
   __syncthreads();
