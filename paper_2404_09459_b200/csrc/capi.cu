@@ -233,6 +233,8 @@ int rgsv_svd_vectors_blocked(double* v, int64_t ldv, int nv, int len, double* ac
                              double* sv, double* xn, int64_t ldx, double* jo, int64_t ldj,
                              int ascending, int* nzero, int* status, void* workspace,
                              size_t workspace_bytes, void* stream) {
+  if (ldv < len || ldacc < nv || ldx < len || ldj < nv) return RGSV_ERR_DIMENSION;
+  if (!v || !acc || !sv || !xn || !jo || !nzero || !status) return RGSV_ERR_VALIDATION;
   return svd_vectors_blocked(v, ldv, nv, len, acc, ldacc, sv, xn, ldx, jo, ldj, ascending, nzero,
                              status, workspace, workspace_bytes,
                              reinterpret_cast<cudaStream_t>(stream));
@@ -666,7 +668,9 @@ int rgsv_dense_qr(const double* a1, int64_t lda1, int m1, const double* a2, int6
   if (m1 < 0 || m2 < 0 || N < 1 || m1 + m2 < 1 || m1 + m2 > kHhMaxRows) return RGSV_ERR_DIMENSION;
   if ((m2 > 0 && !a2) || !a1 || !q) return RGSV_ERR_VALIDATION;
   const int K = (m1 + m2) < N ? (m1 + m2) : N;
-  if (ldq < K || (r && ldr < N)) return RGSV_ERR_DIMENSION;
+  if (ldq < K || (r && ldr < N) || (m1 > 0 && lda1 < N) || (m2 > 0 && lda2 < N))
+    return RGSV_ERR_DIMENSION;
+  if (!workspace || workspace_bytes < hhqr_workspace_bytes(m1 + m2, N)) return RGSV_ERR_WORKSPACE;
   return hhqr(a1, lda1, m1, a2, lda2, m2, N, q, ldq, r, ldr, phase_fix, workspace,
               workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
@@ -702,6 +706,10 @@ int rgsv_spectrum_from_l_blocks(const double* l1b, int64_t ld1, int l1, const do
                                 void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (l1 < 0 || l2 < 0 || cols < 0 || n < 1 || branch < 0 || branch > 2) return RGSV_ERR_DIMENSION;
+  // the singular-value counts min(l, cols) must fit the n-long spectrum
+  if ((l1 > 0 && ld1 < cols) || (l2 > 0 && ld2 < cols) || (l1 < cols ? l1 : cols) > n ||
+      (l2 < cols ? l2 : cols) > n)
+    return RGSV_ERR_DIMENSION;
   if (!(classify_tol > 0.0 && classify_tol < 1e-2)) return RGSV_ERR_VALIDATION;
   if (workspace_bytes < rgsv_spectrum_from_l_blocks_workspace_bytes(l1, l2, cols, n))
     return RGSV_ERR_WORKSPACE;
@@ -814,6 +822,7 @@ int rgsv_gemm_gx(const double* a, int64_t lda, const double* bt, int64_t ldb, do
 
 int rgsv_gemm_gram_lower(const double* a, int64_t lda, int64_t cols, int64_t rows, double* c,
                          int64_t ldc, void* scratch, size_t scratch_bytes, void* stream) {
+  if (cols < 1 || rows < 1 || lda < cols || ldc < cols) return RGSV_ERR_DIMENSION;
   GemmArgs g;
   g.A = a;
   g.lda = lda;

@@ -69,3 +69,28 @@ def test_error_mapping():
         _native.check(5, "x")
     assert errors.ConvergenceError.category == "numerical"
     assert errors.RecoveryError.category == "recovery"
+
+
+def test_round2_entry_points_reject_bad_arguments_without_launch():
+    """The round-2 entry points validate shapes before touching the device."""
+    from paper_2404_09459_b200 import _native
+
+    lib = _native.lib()
+    null = None
+    # rgsv_dense_qr: too many rows, bad leading dimensions, missing workspace
+    assert lib.rgsv_dense_qr(null, 10, 1409, null, 0, 0, 10, null, 10, null, 0, 1, null, 0,
+                             null) == 1
+    assert lib.rgsv_dense_qr(null, 4, 8, null, 0, 0, 10, null, 8, null, 0, 1, null, 0,
+                             null) == 2  # a1 is NULL -> validation error
+    assert lib.rgsv_dense_qr_workspace_bytes(1409, 10) == 0
+    # rgsv_spectrum_from_l_blocks: bad branch, classify_tol, ld < cols
+    assert lib.rgsv_spectrum_from_l_blocks(null, 4, 2, null, 4, 2, 4, 8, 1e-10, 3, null, null,
+                                           null, null, null, 0, null) == 1
+    assert lib.rgsv_spectrum_from_l_blocks(null, 4, 2, null, 4, 2, 4, 8, 0.5, 0, null, null,
+                                           null, null, null, 0, null) == 2
+    assert lib.rgsv_spectrum_from_l_blocks(null, 3, 2, null, 4, 2, 4, 8, 1e-10, 0, null, null,
+                                           null, null, null, 1 << 20, null) == 1
+    # rgsv_svd_vectors_blocked / rgsv_gemm_gram_lower: leading dimensions
+    assert lib.rgsv_svd_vectors_blocked(null, 3, 4, 8, null, 4, null, null, 8, null, 4, 0, null,
+                                        null, null, 0, null) == 1
+    assert lib.rgsv_gemm_gram_lower(null, 10, 16, 100, null, 8, null, 0, null) == 1
