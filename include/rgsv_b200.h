@@ -49,6 +49,7 @@ extern "C" {
 #define RGSV_ST_DEGENERATE 0x10     /* vanishing alpha/beta energy (analysis.py:58-59) */
 #define RGSV_ST_NOT_NORMALIZED 0x20 /* |sum p - 1| > 1e-10 (analysis.py:74-75) */
 #define RGSV_ST_OMEGA_SHORT 0x40    /* Omega generator ran out of raw draws (never expected) */
+#define RGSV_ST_SPECTRUM 0x80       /* GsvSpectrum invariant violated (engine.py:108-125; batch path) */
 
 const char* rgsv_version(void);
 

@@ -29,6 +29,7 @@ OK, ERR_DIMENSION, ERR_VALIDATION, ERR_RANK, ERR_CONVERGENCE, ERR_CUDA, ERR_WORK
 ST_CHOL, ST_NONFINITE, ST_JACOBI, ST_CLASSIFY, ST_DEGENERATE, ST_NOT_NORMALIZED = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
 ST_OMEGA_SHORT = 0x40
+ST_SPECTRUM = 0x80  # GsvSpectrum invariant violated (k_batch_small)
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64

@@ -129,7 +129,7 @@ struct Layout {
   static constexpr int kX = KP * GP;                // X^T (KP x NP)
   static constexpr int kPart = NP * KP;             // one reduction slot
   static constexpr int kSmall = KP * (KP + 1);      // Gram / L / L^-1
-  static_assert(NP * KP + kWarps * 64 <= kG, "zb + wred must fit the idle G ring");
+  static_assert(NP * KP + kWarps * 3 * 64 <= kG, "zb + wred must fit the idle G ring");
   static size_t bytes(int yrows) {
     return sizeof(double) * ((size_t)yrows * KP + kG + kX + 2 * kPart + 3 * kSmall + 64);
   }
@@ -310,7 +310,7 @@ struct Chain {
     constexpr int kB = (KP / 8) * (KP / 8);
     const int nks = (rows + 3) / 4;
     double* dst = slot_ptr();
-    if (kB >= kWarps) {
+    if constexpr (kB >= kWarps) {
       for (int b = warp; b < kB; b += kWarps) {
         const int ib = b % (KP / 8), jb = b / (KP / 8);
         double c[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
@@ -332,38 +332,50 @@ struct Chain {
         dst[r * KP + col + 1] = c[1];
       }
       return;
-    }
-    // kB = 4 (KP = 16): warp -> block (warp % 4), k-steps split by warp / 4
-    const int b = warp % kB, half = warp / kB;
-    const int ib = b % (KP / 8), jb = b / (KP / 8);
-    constexpr int kStep = kWarps / kB;
-    double c[4][2] = {};
-    int ks = half;
-    for (; ks + 3 * kStep < nks; ks += 4 * kStep) {
+    } else {
+    // KP = 16: the Gram is symmetric, so only the three 8 x 8 blocks on and
+    // below the diagonal are multiplied ((0,0), (1,0), (1,1)); warp w takes
+    // the k-steps w, w + 8, ... of all three and the 8 warp partials are
+    // folded in a fixed order. The strictly upper block is the mirror (the
+    // same products in the same order, so the Gram stays exactly symmetric).
+    static_assert(KP == 16 && kWarps == 8, "lower-block Gram layout");
+    const int g = lane >> 2, t = lane & 3;
+    double c[3][2][2] = {};
+    // two k-steps per iteration into separate accumulators (independent
+    // DMMA chains); rows are a multiple of 32, so nks is a multiple of 8
+    for (int ks = warp; ks < nks; ks += 2 * kWarps) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = (ks + u * kStep) * 4 + (lane & 3);
-        dmma(c[u], buf[yx<KP>(rr, ib * 8 + (lane >> 2))], buf[yx<KP>(rr, jb * 8 + (lane >> 2))]);
+      for (int u = 0; u < 2; ++u) {
+        if (ks + u * kWarps < nks) {
+          const int rr = (ks + u * kWarps) * 4 + t;
+          const double y0 = buf[yx<KP>(rr, g)], y1 = buf[yx<KP>(rr, 8 + g)];
+          dmma(c[0][u], y0, y0);
+          dmma(c[1][u], y1, y0);
+          dmma(c[2][u], y1, y1);
+        }
       }
     }
-    for (; ks < nks; ks += kStep) {
-      const int rr = ks * 4 + (lane & 3);
-      dmma(c[0], buf[yx<KP>(rr, ib * 8 + (lane >> 2))], buf[yx<KP>(rr, jb * 8 + (lane >> 2))]);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      wred[(warp * 3 + b) * 64 + lane * 2] = c[b][0][0] + c[b][1][0];
+      wred[(warp * 3 + b) * 64 + lane * 2 + 1] = c[b][0][1] + c[b][1][1];
     }
-    c[0][0] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
-    c[0][1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
-    wred[warp * 64 + lane * 2] = c[0][0];
-    wred[warp * 64 + lane * 2 + 1] = c[0][1];
     __syncthreads();
-    if (warp < kB) {
+    if (warp < 3) {
       double s0 = 0.0, s1 = 0.0;
-      for (int h = 0; h < kWarps / kB; ++h) {  // fixed order
-        s0 += wred[(warp + h * kB) * 64 + lane * 2];
-        s1 += wred[(warp + h * kB) * 64 + lane * 2 + 1];
+      for (int w = 0; w < kWarps; ++w) {  // fixed order
+        s0 += wred[(w * 3 + warp) * 64 + lane * 2];
+        s1 += wred[(w * 3 + warp) * 64 + lane * 2 + 1];
       }
-      const int r = ib * 8 + (lane >> 2), col = jb * 8 + 2 * (lane & 3);
+      const int ib = warp == 0 ? 0 : 1, jb = warp == 2 ? 1 : 0;
+      const int r = ib * 8 + g, col = jb * 8 + 2 * t;
       dst[r * KP + col] = s0;
       dst[r * KP + col + 1] = s1;
+      if (ib != jb) {
+        dst[col * KP + r] = s0;
+        dst[(col + 1) * KP + r] = s1;
+      }
+    }
     }
   }
 
@@ -386,6 +398,11 @@ struct Chain {
 #ifdef RGSV_BATCH_PROFILE
       if (tid == 0) atomicAdd(&g_batch_prof[13], (unsigned long long)(clock64() - _c0));
 #endif
+      return;
+    }
+    if constexpr (KP == 16) {
+      if (warp == 0) chol16(k, shift_rows);
+      __syncthreads();
       return;
     }
     if (warp == 0) {
@@ -456,6 +473,63 @@ struct Chain {
 #endif
     }
     __syncthreads();
+  }
+
+  // ---- the same symmetric Gauss-Jordan for KP = 16 on the whole warp:
+  //      lanes 0-15 hold row `lane` of A, lanes 16-31 row `lane - 16` of the
+  //      augmented identity X, so every lane updates 16 entries per pivot
+  //      (not 32) and one 16-shuffle broadcast of the pivot row serves both
+  //      halves (each half reads its own pivot lane). Same operations in the
+  //      same order per entry as the one-half form.
+  RGSV_DI void chol16(int k, int64_t shift_rows) {
+    constexpr int LD = KP + 1;
+    const int row = lane & 15;
+    const bool isx = lane >= 16;
+    const bool row_ok = !isx && row < k;
+    double v[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      v[c] = (row_ok && c < k) ? gram[row * LD + c] : (row == c ? 1.0 : 0.0);
+    if (shift_rows > 0) {
+      double dg = 0.0;
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c == row && row_ok) dg = v[c];
+      const double tr = warp_sum(dg);
+      const double sh = 11.0 * ((double)shift_rows * k + (double)k * (k + 1)) * 0x1p-53 * tr;
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c == row && row_ok) v[c] += sh;
+    }
+    bool bad = false;
+    const int src_half = isx ? 16 : 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const double d = __shfl_sync(0xffffffffu, v[j], j);
+      const double aij = __shfl_sync(0xffffffffu, v[j], row);  // A[row][j] (own for A lanes)
+      double pv[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) pv[c] = __shfl_sync(0xffffffffu, v[c], src_half + j);
+      bad |= !(d > 0.0) || !isfinite(d);
+      const double r = rsqrt(d);
+      const double ff = (row > j) ? aij * (r * r) : 0.0;
+      const double mul = (row == j) ? r : 1.0;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (c > j) {
+          if (!isx) v[c] = fma(-ff, pv[c], v[c]) * mul;
+        } else {
+          if (isx) v[c] = fma(-ff, pv[c], v[c]) * mul;
+        }
+      }
+      if (!isx) v[j] = (row > j) ? 0.0 : (row == j ? d * r : v[j]);
+    }
+    if (bad) fail = 1;
+    if (isx) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        linv[row * LD + c] = bad ? (row == c ? 1.0 : 0.0) : (c <= row ? v[c] : 0.0);
+    }
   }
 
   // ---- third CholeskyQR pass: gram = I + E with max|E| <= 1e-6 ->
@@ -544,12 +618,15 @@ struct Chain {
       }
       __syncwarp();
       double c[2][KP / 8][2] = {};
+      // L^-1 is lower triangular: output column block cb only sees the
+      // k-steps ks <= 2 cb + 1 (the skipped products are exact zeros)
 #pragma unroll
       for (int ks = 0; ks < KP / 4; ++ks)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int cb = 0; cb < KP / 8; ++cb) dmma(c[h][cb], a[h][ks], lf[cb][ks]);
+          for (int cb = 0; cb < KP / 8; ++cb)
+            if (ks <= 2 * cb + 1) dmma(c[h][cb], a[h][ks], lf[cb][ks]);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (rb0 + h >= nrb) break;
@@ -567,7 +644,12 @@ struct Chain {
 
   // ---- shifted CholeskyQR3 of a row-sharded slice (cluster Gram) or of a
   //      replicated small matrix (local Gram, no cluster traffic)
-  RGSV_DI void cholqr3(double* buf, int rows, int k, int64_t shift_rows, bool sharded) {
+  //      defer_last: the third pass stops after its Cholesky -- buf keeps
+  //      Q2 and linv holds L3^-1 -- because the only consumer of Q is the
+  //      next G^T Q pass: G^T (Q2 L3^-T) = (G^T Q2) L3^-T is applied to the
+  //      reduced n x k product instead of the m x k slice.
+  RGSV_DI void cholqr3(double* buf, int rows, int k, int64_t shift_rows, bool sharded,
+                       bool defer_last = false) {
     constexpr int LD = KP + 1;
     PROF_T0();
     for (int pass = 0; pass < 3; ++pass) {
@@ -584,6 +666,7 @@ struct Chain {
       PROF(5);
       chol(k, pass == 0 ? shift_rows : 0);
       PROF(6);
+      if (defer_last && pass == 2) break;
       trsm(buf, rows);
       PROF(7);
     }
@@ -633,13 +716,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       C.reduce(1, [&](int, double s) { C.misc[0] = s; });
     }
     PROF(8);
-    C.cholqr3(C.ys, rlt, k, rows, true);
+    C.cholqr3(C.ys, rlt, k, rows, true, true);
     PROF(9);
     for (int it = 0; it < A.q; ++it) {
       // (2) Z = G^T Q (n x k), cluster-reduced, then Qhat = cholqr3(Z)
       C.pass_gtq(g, r0, r1, n);
       PROF(2);
       C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
+      C.trsm(C.zb, NP);  // the deferred L3^-T of Q
       PROF(10);
       C.cholqr3(C.zb, NP, k, n, false);
       PROF(11);
@@ -652,20 +736,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       C.pass_gx(g, r0, r1, n, nullptr);
       __syncthreads();
       PROF(1);
-      C.cholqr3(C.ys, rlt, k, rows, true);
+      C.cholqr3(C.ys, rlt, k, rows, true, true);
       PROF(9);
     }
     // (4) B^T = G^T Q (n x k), cluster-reduced; rank 0 writes B and ||B||^2
     C.pass_gtq(g, r0, r1, n);
     PROF(2);
-    C.reduce(NP * KP, [&](int e, double s) { C.zb[e] = s; });
+    C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
+    C.trsm(C.zb, NP);  // the deferred L3^-T of Q
     PROF(10);
     if (C.crank == 0) {
       double* bo = A.b_out + (int64_t)mat * A.b_stride;
       double e2 = 0.0;
       for (int e = C.tid; e < KP * n; e += kThreads) {
         const int i = e / n, j = e % n;
-        const double v = (i < k) ? C.zb[j * KP + i] : 0.0;
+        const double v = (i < k) ? C.zb[yx<KP>(j, i)] : 0.0;
         bo[(int64_t)i * A.ldb + j] = v;
         e2 = fma(v, v, e2);
       }

@@ -1044,6 +1044,22 @@ __global__ void __launch_bounds__(256) k_batch_small(const double* __restrict__ 
   comparative_body(sv, nsv, sv + 64, n, tol, o, o + n, o + 2 * n, o + 3 * n, o + 4 * n,
                    o + 5 * n, o + 6 * n, ints + 4 * j + 2, st, red);
   __syncthreads();
+  // GsvSpectrum invariants (engine.py:108-125) checked here, so the host
+  // reads one status word per pair instead of re-scanning every spectrum;
+  // the same arithmetic as the host checks (no FMA contraction)
+  if (!(*(volatile int*)st & (RGSV_ST_CLASSIFY | RGSV_ST_DEGENERATE))) {
+    const int r = ints[4 * j + 2], s = ints[4 * j + 3];
+    int bad = (r < 0 || s < 0 || r + s > n) ? 1 : 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double a = o[i], bb = o[n + i];
+      bad |= !(a >= 0.0 && a <= 1.0 && bb >= 0.0 && bb <= 1.0);
+      if (i + 1 < n)
+        bad |= (__dsub_rn(o[i + 1], a) > 1e-12) | (__dsub_rn(o[n + i + 1], bb) < -1e-12);
+      bad |= !(fabs(__dsub_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(bb, bb)), 1.0)) <= 1e-12);
+      bad |= (i < r && bb != 0.0) | (i >= r + s && a != 0.0);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(st, RGSV_ST_SPECTRUM);
+  }
   for (int i = threadIdx.x; i < k1; i += blockDim.x) o[6 * n + 4 + i] = sv[i];
   for (int i = threadIdx.x; i < k2; i += blockDim.x) o[6 * n + 4 + k1 + i] = sv[64 + i];
   if (threadIdx.x == 0) {

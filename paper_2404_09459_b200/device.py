@@ -655,10 +655,16 @@ class SmallBatchPlan:
                                     vp(self.ws), self.ws_bytes, sp(st)), "rgsv_batch_gsvd")
 
     def fetch(self):
-        self.fhost.copy_(self.fbuf, non_blocking=True)
-        self.ihost.copy_(self.ibuf, non_blocking=True)
+        """One packed D2H of the results into FRESH pinned buffers (torch's
+        caching host allocator recycles them once the caller drops the
+        previous results), returned as numpy views: nothing is copied on the
+        host, and earlier results stay valid."""
+        fh = torch.empty(self.fbuf.shape, dtype=F64, pin_memory=True)
+        ih = torch.empty(self.ibuf.shape, dtype=torch.int32, pin_memory=True)
+        fh.copy_(self.fbuf, non_blocking=True)
+        ih.copy_(self.ibuf, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        return self.fhost.numpy(), self.ihost.numpy()
+        return fh.numpy(), ih.numpy()
 
     def run(self, pairs, seeds, q_iters: int, classify_tol: float):
         self.set_pairs(pairs)

@@ -139,3 +139,36 @@ def test_host_stream_batch_equals_resident(rg):
     bad[0][0][3, 4] = np.nan
     with pytest.raises(rg.ValidationError):
         rg.compare_batch(bad, opts, [0])
+
+
+def test_batch_results_survive_later_calls_and_flag_bad_input(rg):
+    """Each compare_batch call returns views of its OWN pinned result
+    buffers: a second call (new seeds, new pair set) leaves the first
+    call's reports untouched. The device-side status word carries the
+    finiteness and GsvSpectrum checks: a NaN in one pair's G raises
+    ValidationError; a shape mismatch raises DimensionError."""
+    cfg = CONFIGS["cfg3"]
+    hosts, pairs, seeds = _pairs(rg, cfg, 4, m=900, p=700)
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(cfg.k, 0, cfg.q))
+    first = rg.compare_batch(pairs, opts, seeds)
+    keep = [(r.theta.copy(), r.d1, r.spectrum.alphas.copy()) for r in first]
+    second = rg.compare_batch(pairs[::-1], opts, [s + 100 for s in seeds])
+    assert len(second) == 4
+    for r, (th, d1, al) in zip(first, keep):
+        assert np.array_equal(r.theta, th) and r.d1 == d1 and np.array_equal(r.spectrum.alphas, al)
+    for j, (g1, g2) in enumerate(hosts):  # both calls still match the oracle
+        o = orc.run_pipeline(g1, g2, k=cfg.k, q=cfg.q, seed=seeds[j])
+        assert np.array_equal(first[j].spectrum.alphas, o.alphas)
+        o2 = orc.run_pipeline(g1, g2, k=cfg.k, q=cfg.q, seed=seeds[j] + 100)
+        assert np.array_equal(second[3 - j].spectrum.alphas, o2.alphas)
+        assert abs(second[3 - j].d2 - orc.comparative(o2.alphas, o2.betas, o2.r)[5]) <= 1e-12
+    bad_g = pairs[2].g1.t.clone()
+    bad_g[5, 7] = float("nan")
+    bad = list(pairs)
+    bad[2] = rg.GmpPair.resident(bad_g, pairs[2].g2.t)
+    with pytest.raises(rg.ValidationError):
+        rg.compare_batch(bad, opts, seeds)
+    odd = list(pairs)
+    odd[1] = rg.GmpPair.resident(pairs[1].g1.t[:800], pairs[1].g2.t)
+    with pytest.raises(rg.DimensionError):
+        rg.compare_batch(odd, opts, seeds)

@@ -181,9 +181,32 @@ def test_small_batch_runs_reject(corrupt, exc):
         ih[4 * 3 + 2] = 0x4
     elif corrupt == "nonfinite":
         fh[3 * rs + 4] = np.nan
+    if corrupt in ("pythagoras", "order", "unsnapped"):
+        ih[4 * 3 + 1] = 0x80  # RGSV_ST_SPECTRUM: k_batch_small's device-side check
     exc = getattr(rg, exc) if isinstance(exc, str) else exc
     with pytest.raises(exc):
         SmallBatchRuns(fh, ih, plan, GsvOptions(extraction=ExtractionConfig.fixed_rank(2)))
+
+
+def test_small_batch_runs_spectrum_message_and_nan():
+    """The host re-scan behind RGSV_ST_SPECTRUM names the violated invariant
+    with the reference's message; a NaN spectrum (no numpy comparison
+    catches it) still raises."""
+    from paper_2404_09459_b200.engine import SmallBatchRuns
+
+    opts = GsvOptions(extraction=ExtractionConfig.fixed_rank(2))
+    fh, ih, plan = _fake_batch()
+    n, rs = plan.n, plan.res_stride
+    fh[rs + n] = 1e-300  # classified-zero beta that is not exactly 0
+    fh[rs] = math.sqrt(1 - 1e-600)
+    ih[4 * 3 + 1] = 0x80
+    with pytest.raises(ValidationError, match="classified-zero"):
+        SmallBatchRuns(fh, ih, plan, opts)
+    fh, ih, plan = _fake_batch()
+    fh[2 * rs] = np.nan  # alpha_0 of pair 2
+    ih[4 * 3 + 2] = 0x80
+    with pytest.raises(ValidationError, match="GSVs must lie"):
+        SmallBatchRuns(fh, ih, plan, opts)
 
 
 def test_bench_reference_arm_contract():
