@@ -418,16 +418,18 @@ def extract_basis(g, cfg: ExtractionConfig | None = None, *, device_result: bool
     return BasisResult(q if device_result else q.cpu().numpy(), hist, hist[-1] < tol, 1, [width])
 
 
-def residual_norm(g, q) -> float:
-    """Explicit ||(I - QQ^H)G||_F on the device (rangefinder.py:138-154)."""
-    a = _dev.to_device(g, "g")
+def projected(a: "_dev.DevMatrix", q) -> torch.Tensor:
+    """Q (Q^T G) on the device (two DMMA GEMMs): the rows x cols projection
+    of G onto the basis' range, as residual_norm (rangefinder.py:138-154)
+    and the CLI's bounds command (cli.py:164-165) form it."""
     qa = q if isinstance(q, torch.Tensor) else torch.from_numpy(np.asarray(q, dtype=np.float64))
     if qa.dim() != 2:
         raise DimensionError(f"q must be 2-D, got shape {tuple(qa.shape)}")
     if qa.shape[0] != a.rows:
         raise DimensionError(f"q has {qa.shape[0]} rows but g has {a.rows}")
+    proj = torch.zeros((a.rows, a.cols + (a.cols & 1)), dtype=torch.float64, device="cuda")
     if qa.shape[1] == 0:
-        return math.sqrt(_dev.device_sumsq(a))
+        return proj[:, : a.cols]
     L = lib()
     qd = qa.to("cuda", torch.float64)
     l = qd.shape[1]
@@ -444,11 +446,17 @@ def residual_norm(g, q) -> float:
                           a.rows, _dev.vp(scratch), scratch.numel() * 8, st), "Q^T G")
     bt = torch.zeros((a.cols + (a.cols & 1), lp), dtype=torch.float64, device="cuda")
     bt[: a.cols, :] = b[:, : a.cols].t()
-    proj = torch.zeros((a.rows, a.ld), dtype=torch.float64, device="cuda")
     # QQ^T G = Q (Q^T G): gx with A = Q (rows x lp), Bt = (Q^T G)^T (cols x lp)
-    check(L.rgsv_gemm_gx(_dev.vp(qp), lp, _dev.vp(bt), lp, _dev.vp(proj), a.ld, a.rows, a.cols,
-                         lp, _dev.vp(scratch), scratch.numel() * 8, st), "Q (Q^T G)")
-    resid = _dev.DevMatrix((a.t - proj[:, : a.cols]).contiguous(), a.rows, a.cols)
+    check(L.rgsv_gemm_gx(_dev.vp(qp), lp, _dev.vp(bt), lp, _dev.vp(proj), proj.stride(0), a.rows,
+                         a.cols, lp, _dev.vp(scratch), scratch.numel() * 8, st), "Q (Q^T G)")
+    return proj[:, : a.cols]
+
+
+def residual_norm(g, q) -> float:
+    """Explicit ||(I - QQ^H)G||_F on the device (rangefinder.py:138-154)."""
+    a = _dev.to_device(g, "g")
+    proj = projected(a, q)
+    resid = _dev.DevMatrix((a.t - proj).contiguous(), a.rows, a.cols)
     return math.sqrt(_dev.device_sumsq(resid))
 
 
