@@ -401,7 +401,7 @@ struct Chain {
       return;
     }
     if constexpr (KP == 16) {
-      if (warp == 0) chol16(k, shift_rows);
+      chol16(k, shift_rows);
       __syncthreads();
       return;
     }
@@ -475,61 +475,64 @@ struct Chain {
     __syncthreads();
   }
 
-  // ---- the same symmetric Gauss-Jordan for KP = 16 on the whole warp:
-  //      lanes 0-15 hold row `lane` of A, lanes 16-31 row `lane - 16` of the
-  //      augmented identity X, so every lane updates 16 entries per pivot
-  //      (not 32) and one 16-shuffle broadcast of the pivot row serves both
-  //      halves (each half reads its own pivot lane). Same operations in the
-  //      same order per entry as the one-half form.
+  // ---- the same symmetric Gauss-Jordan for KP = 16 on the whole CTA: thread
+  //      (i, c) = (tid / 16, tid % 16) owns A[i][c] and X[i][c] in registers.
+  //      Per pivot j it needs the pivot row (A[j][c], X[j][c]), its own row's
+  //      column-j entry A[i][j] and d = A[j][j]: every thread publishes its
+  //      two entries in a double-buffered shared-memory copy, so one CTA
+  //      barrier per pivot suffices. The j loop is NOT unrolled: the body is
+  //      ~60 instructions that stay in the instruction cache (the unrolled
+  //      one-warp form was 2500 instructions per call site, executed once per
+  //      call, i.e. instruction-fetch bound: 9.5 us per call). Same operations
+  //      in the same order per entry as the one-warp form (bitwise equal).
   RGSV_DI void chol16(int k, int64_t shift_rows) {
     constexpr int LD = KP + 1;
-    const int row = lane & 15;
-    const bool isx = lane >= 16;
-    const bool row_ok = !isx && row < k;
-    double v[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c)
-      v[c] = (row_ok && c < k) ? gram[row * LD + c] : (row == c ? 1.0 : 0.0);
+    static_assert(kThreads == 256, "one thread per entry of the 16 x 16 pivot");
+    const int i = tid >> 4, c = tid & 15;
+    double a = (i < k && c < k) ? gram[i * LD + c] : (i == c ? 1.0 : 0.0);
+    double x = (i == c) ? 1.0 : 0.0;
+    // double-buffered copies: [buf][A | X][16 x LD] in lmat / the idle wred
+    double* pub = wred;  // 2 x 2 x 16 x LD = 1088 doubles <= kWarps * 3 * 64
+    static_assert(4 * 16 * (KP + 1) <= kWarps * 3 * 64, "chol16 buffers fit wred");
     if (shift_rows > 0) {
-      double dg = 0.0;
+      if (tid < 16) lmat[tid] = (tid < k) ? gram[tid * LD + tid] : 0.0;
+      __syncthreads();
+      // trace in the order of the one-warp form's xor butterfly (8, 4, 2, 1)
+      double t8[16];
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c == row && row_ok) dg = v[c];
-      const double tr = warp_sum(dg);
+      for (int e = 0; e < 16; ++e) t8[e] = lmat[e];
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+        for (int e = 0; e < o; ++e) t8[e] = t8[e] + t8[e + o];
+      const double tr = t8[0];
       const double sh = 11.0 * ((double)shift_rows * k + (double)k * (k + 1)) * 0x1p-53 * tr;
-#pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c == row && row_ok) v[c] += sh;
+      if (i == c && i < k) a += sh;
+      __syncthreads();
     }
     bool bad = false;
-    const int src_half = isx ? 16 : 0;
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < 16; ++j) {
-      const double d = __shfl_sync(0xffffffffu, v[j], j);
-      const double aij = __shfl_sync(0xffffffffu, v[j], row);  // A[row][j] (own for A lanes)
-      double pv[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) pv[c] = __shfl_sync(0xffffffffu, v[c], src_half + j);
+      double* pa = pub + (j & 1) * (2 * 16 * LD);
+      double* px = pa + 16 * LD;
+      pa[i * LD + c] = a;
+      px[i * LD + c] = x;
+      __syncthreads();
+      const double d = pa[j * LD + j];
+      const double aij = pa[i * LD + j];
+      const double rowa = pa[j * LD + c];
+      const double rowx = px[j * LD + c];
       bad |= !(d > 0.0) || !isfinite(d);
       const double r = rsqrt(d);
-      const double ff = (row > j) ? aij * (r * r) : 0.0;
-      const double mul = (row == j) ? r : 1.0;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (c > j) {
-          if (!isx) v[c] = fma(-ff, pv[c], v[c]) * mul;
-        } else {
-          if (isx) v[c] = fma(-ff, pv[c], v[c]) * mul;
-        }
-      }
-      if (!isx) v[j] = (row > j) ? 0.0 : (row == j ? d * r : v[j]);
+      const double ff = (i > j) ? aij * (r * r) : 0.0;
+      const double mul = (i == j) ? r : 1.0;
+      if (c > j) a = fma(-ff, rowa, a) * mul;
+      else x = fma(-ff, rowx, x) * mul;
+      if (c == j) a = (i > j) ? 0.0 : (i == j ? d * r : a);
     }
     if (bad) fail = 1;
-    if (isx) {
-#pragma unroll
-      for (int c = 0; c < 16; ++c)
-        linv[row * LD + c] = bad ? (row == c ? 1.0 : 0.0) : (c <= row ? v[c] : 0.0);
-    }
+    __syncthreads();  // wred (pub) is reused by the callers right after
+    linv[i * LD + c] = bad ? (i == c ? 1.0 : 0.0) : (c <= i ? x : 0.0);
   }
 
   // ---- third CholeskyQR pass: gram = I + E with max|E| <= 1e-6 ->
@@ -697,54 +700,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
     }
     for (int e = C.tid; e < A.yrows * KP; e += kThreads) C.ys[e] = 0.0;
     __syncthreads();
-    // (1) sketch Y = G Omega, ||G||^2 on the side
+    // One textual instance of every phase (the chain used to inline three
+    // cholqr3 and two bodies of each pass: 315 KB of code run once per
+    // matrix, i.e. instruction-fetch bound). Half-steps: even = the tall side
+    // (Y = G X with X = Omega or Qhat, CholeskyQR3 of the Y slice, then
+    // G^T Q reduced over the cluster with the deferred L3^-T applied: Z, or
+    // B^T on the last half-step), odd = the small side (Qhat = cholqr3(Z)).
     double ss = 0.0;
     PROF(0);
-    C.pass_gx(g, r0, r1, n, &ss);
-    __syncthreads();
-    PROF(1);
-    // ||G||_F^2: block partial in fixed order -> cluster sum
-    {
-      double v = warp_sum(ss);
-      if (C.lane == 0) C.wred[C.warp * 64] = v;
-      __syncthreads();
-      if (C.tid == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s += C.wred[w * 64];
-        C.slot_ptr()[0] = s;
+    const int last = 2 * A.q;
+#pragma unroll 1
+    for (int hs = 0;; ++hs) {
+      const bool tall = (hs & 1) == 0;
+      if (tall) {
+        if (hs > 0) {
+          for (int e = C.tid; e < KP * NP; e += kThreads) {
+            const int i = e / NP, j = e % NP;
+            C.xt[i * C.GP + j] = (j < n) ? C.zb[yx<KP>(j, i)] : 0.0;
+          }
+          __syncthreads();
+        }
+        C.pass_gx(g, r0, r1, n, hs == 0 ? &ss : nullptr);
+        __syncthreads();
+        PROF(1);
+        if (hs == 0) {  // ||G||_F^2: block partial in fixed order -> cluster sum
+          double v = warp_sum(ss);
+          if (C.lane == 0) C.wred[C.warp * 64] = v;
+          __syncthreads();
+          if (C.tid == 0) {
+            double s = 0.0;
+            for (int w = 0; w < kWarps; ++w) s += C.wred[w * 64];
+            C.slot_ptr()[0] = s;
+          }
+          C.reduce(1, [&](int, double s) { C.misc[0] = s; });
+          PROF(8);
+        }
       }
-      C.reduce(1, [&](int, double s) { C.misc[0] = s; });
-    }
-    PROF(8);
-    C.cholqr3(C.ys, rlt, k, rows, true, true);
-    PROF(9);
-    for (int it = 0; it < A.q; ++it) {
-      // (2) Z = G^T Q (n x k), cluster-reduced, then Qhat = cholqr3(Z)
-      C.pass_gtq(g, r0, r1, n);
-      PROF(2);
-      C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
-      C.trsm(C.zb, NP);  // the deferred L3^-T of Q
-      PROF(10);
-      C.cholqr3(C.zb, NP, k, n, false);
-      PROF(11);
-      for (int e = C.tid; e < KP * NP; e += kThreads) {
-        const int i = e / NP, j = e % NP;
-        C.xt[i * C.GP + j] = (j < n) ? C.zb[yx<KP>(j, i)] : 0.0;
-      }
-      __syncthreads();
-      // (3) Y = G Qhat, Q = cholqr3(Y)
-      C.pass_gx(g, r0, r1, n, nullptr);
-      __syncthreads();
-      PROF(1);
-      C.cholqr3(C.ys, rlt, k, rows, true, true);
+      C.cholqr3(tall ? C.ys : C.zb, tall ? rlt : NP, k, tall ? rows : n, tall, tall);
       PROF(9);
+      if (tall) {
+        C.pass_gtq(g, r0, r1, n);
+        PROF(2);
+        C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
+        C.trsm(C.zb, NP);  // the deferred L3^-T of Q
+        PROF(10);
+        if (hs == last) break;
+      }
     }
-    // (4) B^T = G^T Q (n x k), cluster-reduced; rank 0 writes B and ||B||^2
-    C.pass_gtq(g, r0, r1, n);
-    PROF(2);
-    C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
-    C.trsm(C.zb, NP);  // the deferred L3^-T of Q
-    PROF(10);
     if (C.crank == 0) {
       double* bo = A.b_out + (int64_t)mat * A.b_stride;
       double e2 = 0.0;
