@@ -88,6 +88,36 @@ RGSV_DI void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// 16-byte / 8-byte read-only global loads that do not allocate in L1 (G is
+// streamed: each byte is used once per pass).
+RGSV_DI void ldg_stream2(double& x, double& y, const double* p) {
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p));
+}
+// ... with an L2 eviction-priority hint: a matrix is read by four passes ~40 us
+// apart while 37 clusters stream ~74 MB of live data through the L2; the first
+// three passes keep their lines (evict_last), the last one marks them dead
+// (evict_first) so finished matrices do not push live ones out.
+RGSV_DI void ldg_stream2(double& x, double& y, const double* p, uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(x), "=d"(y)
+               : "l"(p), "l"(pol));
+}
+RGSV_DI uint64_t l2_policy(bool keep) {
+  uint64_t pol;
+#ifdef RGSV_BATCH_NOHINT  // A/B builds: every pass with the default priority
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+#endif
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+RGSV_DI double ldg_stream1(const double* p) {
+  double x;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(x) : "l"(p));
+  return x;
+}
+
 // Y / Z slice layout: row-major, pitch KP doubles, XOR swizzle inside each
 // 16-column group so both DMMA fragment patterns used on it (A: 8 rows x 4
 // cols; B: 4 rows x 8 cols) hit the minimum two shared-memory wavefronts.
@@ -228,8 +258,196 @@ struct Chain {
     __syncthreads();
   }
 
+  // ---- register-streamed passes (NP = 64, KP = 16: the cfg3 shape). G goes
+  //      from global memory (L2 after the first pass) straight into DMMA
+  //      fragments, with no shared-memory ring and no CTA barrier inside the
+  //      pass: warp w owns the 8-row blocks w, w + 8, ... of the slice and
+  //      keeps kDepth blocks (4 KB each) in flight in registers, ~64-96 KB per
+  //      SM against the ring's 32 KB, which was latency bound at 14 B/clk/SM.
+  //      16-byte loads fix a permutation of the contraction (gx) / output row
+  //      (gtq) index inside each group of 8 / 16 columns; both operands use
+  //      the same one, and the order of every sum is fixed.
+  static constexpr bool kRegStream = (NP == 64 && KP == 16);
+#ifndef RGSV_BATCH_DGX
+#define RGSV_BATCH_DGX 3
+#endif
+#ifndef RGSV_BATCH_DGTQ
+#define RGSV_BATCH_DGTQ 2
+#endif
+
+  // Y[8-row block] = G_block X: thread (g, t) loads G[row g][8u + 2t, +1];
+  // k-step 2u + h contracts the columns 8u + 2t + h.
+  RGSV_DI void pass_gx_reg(const BatchMat& g, int r0, int r1, int n, double* ss) {
+    constexpr int NK = NP / 4, NCB = KP / 8, kDepth = RGSV_BATCH_DGX;
+    const int gq = lane >> 2, t = lane & 3;
+    double xf[NCB][NK];
+#pragma unroll
+    for (int cb = 0; cb < NCB; ++cb)
+#pragma unroll
+      for (int sidx = 0; sidx < NK; ++sidx)
+        xf[cb][sidx] = xt[(cb * 8 + gq) * GP + 8 * (sidx >> 1) + 2 * t + (sidx & 1)];
+    const int nblk = (r1 - r0 + 7) / 8;
+    const int cnt = nblk > warp ? (nblk - warp + kWarps - 1) / kWarps : 0;
+    double a[kDepth][NK];
+    const uint64_t pol = l2_policy(true);
+    const double* gbase = g.g + (int64_t)(r0 + gq) * g.ld + 2 * t;
+    const int64_t bstride = 8 * g.ld;
+    auto load = [&](double (&dst)[NK], int i) {
+      const int b = warp + i * kWarps;
+      const double* src = gbase + b * bstride;
+      if (n == NP && r0 + b * 8 + 8 <= r1) {  // whole block, whole rows: no predicates
+#pragma unroll
+        for (int u = 0; u < NP / 8; ++u) ldg_stream2(dst[2 * u], dst[2 * u + 1], src + 8 * u, pol);
+        return;
+      }
+      const int row = r0 + b * 8 + gq;
+      const bool rok = row < r1;
+#pragma unroll
+      for (int u = 0; u < NP / 8; ++u) {
+        const int col = 8 * u + 2 * t;
+        if (rok && col + 1 < n) {
+          ldg_stream2(dst[2 * u], dst[2 * u + 1], src + 8 * u);
+        } else {
+          dst[2 * u] = (rok && col < n) ? ldg_stream1(src + 8 * u) : 0.0;
+          dst[2 * u + 1] = 0.0;
+        }
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d)
+      if (d < cnt) load(a[d], d);
+    double sq = 0.0;
+    for (int i = 0; i < cnt; i += kDepth) {
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        if (i + d < cnt) {
+          double c[NCB][2][2] = {};
+#pragma unroll
+          for (int sidx = 0; sidx < NK; ++sidx)
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) dmma(c[cb][sidx & 1], a[d][sidx], xf[cb][sidx]);
+          if (ss) {
+#pragma unroll
+            for (int sidx = 0; sidx < NK; ++sidx) sq = fma(a[d][sidx], a[d][sidx], sq);
+          }
+          const int r = (warp + (i + d) * kWarps) * 8 + gq;
+#pragma unroll
+          for (int cb = 0; cb < NCB; ++cb) {
+            const int col = cb * 8 + 2 * t;
+            ys[yx<KP>(r, col)] = c[cb][0][0] + c[cb][1][0];
+            ys[yx<KP>(r, col + 1)] = c[cb][0][1] + c[cb][1][1];
+          }
+          if (i + d + kDepth < cnt) load(a[d], i + d + kDepth);
+        }
+      }
+    }
+    if (ss) *ss += sq;
+  }
+
+  // part = G^T Y over this CTA's rows: thread (g, t) loads G[row t][16v + 2g,
+  // +1]; output block 2v + h holds the G columns 16v + 2g + h. Every warp
+  // accumulates the whole NP x KP product over its own rows; the 8 warp
+  // partials are folded in a fixed order through the (idle) ring memory.
+  RGSV_DI void pass_gtq_reg(const BatchMat& g, int r0, int r1, int n, bool final_pass) {
+    constexpr int NV = NP / 16, NJB = KP / 8, SP = KP + 4, kDepth = RGSV_BATCH_DGTQ;  // SP: conflict-free 16 B stores
+    static_assert(4 * NP * SP <= Lo::kG, "warp partials fit the idle ring");
+    const int gq = lane >> 2, t = lane & 3;
+    double acc[2 * NV][NJB][2] = {};
+    const int nblk = (r1 - r0 + 7) / 8;
+    const int cnt = nblk > warp ? (nblk - warp + kWarps - 1) / kWarps : 0;
+    double a[kDepth][2][NV][2];
+    const uint64_t pol = l2_policy(!final_pass);
+    const double* gbase = g.g + (int64_t)(r0 + t) * g.ld + 2 * gq;
+    const int64_t bstride = 8 * g.ld, hstride = 4 * g.ld;
+    auto load = [&](double (&dst)[2][NV][2], int i) {
+      const int b = warp + i * kWarps;
+      if (n == NP && r0 + b * 8 + 8 <= r1) {  // whole block, whole rows: no predicates
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            ldg_stream2(dst[h][v][0], dst[h][v][1], gbase + b * bstride + h * hstride + 16 * v, pol);
+        return;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = r0 + b * 8 + 4 * h + t;
+        const bool rok = row < r1;
+        const double* src = g.g + (int64_t)row * g.ld + 2 * gq;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int col = 16 * v + 2 * gq;
+          if (rok && col + 1 < n) {
+            ldg_stream2(dst[h][v][0], dst[h][v][1], src + 16 * v);
+          } else {
+            dst[h][v][0] = (rok && col < n) ? ldg_stream1(src + 16 * v) : 0.0;
+            dst[h][v][1] = 0.0;
+          }
+        }
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d)
+      if (d < cnt) load(a[d], d);
+    for (int i = 0; i < cnt; i += kDepth) {
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        if (i + d < cnt) {
+          const int rl0 = (warp + (i + d) * kWarps) * 8;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double bf[NJB];
+#pragma unroll
+            for (int jb = 0; jb < NJB; ++jb) bf[jb] = ys[yx<KP>(rl0 + 4 * h + t, jb * 8 + gq)];
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int jb = 0; jb < NJB; ++jb) dmma(acc[2 * v + e][jb], a[d][h][v][e], bf[jb]);
+          }
+          if (i + d + kDepth < cnt) load(a[d], i + d + kDepth);
+        }
+      }
+    }
+    // fold the warp partials: ((w0 + w4) + (w1 + w5)) + ((w2 + w6) + (w3 + w7))
+    double* scr = gst + (warp & 3) * (NP * SP);
+    __syncthreads();  // the ring memory (zb / wred) is no longer read
+#pragma unroll
+    for (int ph = 0; ph < 2; ++ph) {
+      if ((warp >> 2) == ph) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int jb = 0; jb < NJB; ++jb) {
+              double2* q = reinterpret_cast<double2*>(scr + (16 * v + 2 * gq + e) * SP + jb * 8 +
+                                                      2 * t);
+              double2 val = make_double2(acc[2 * v + e][jb][0], acc[2 * v + e][jb][1]);
+              if (ph == 1) {
+                const double2 o = *q;
+                val.x = o.x + val.x;
+                val.y = o.y + val.y;
+              }
+              *q = val;
+            }
+      }
+      __syncthreads();
+    }
+    double* dst = slot_ptr();
+    for (int e = tid; e < NP * KP; e += kThreads) {
+      const int o = (e / KP) * SP + (e % KP);
+      dst[e] = (gst[o] + gst[NP * SP + o]) + (gst[2 * NP * SP + o] + gst[3 * NP * SP + o]);
+    }
+  }
+
   // ---- Y[t-tile] = G_tile X  (pass A); optional sum of squares of G
   RGSV_DI void pass_gx(const BatchMat& g, int r0, int r1, int n, double* ss) {
+    if constexpr (kRegStream) {
+      pass_gx_reg(g, r0, r1, n, ss);
+      return;
+    }
     constexpr int kRB = kTR / 8, kCB = KP / 8, kBlocks = kRB * kCB;
     static_assert(kBlocks % kWarps == 0, "whole blocks per warp");
     constexpr int kPer = kBlocks / kWarps;
@@ -274,7 +492,11 @@ struct Chain {
   }
 
   // ---- part = G^T Y over this CTA's rows (pass B), NP x KP
-  RGSV_DI void pass_gtq(const BatchMat& g, int r0, int r1, int n) {
+  RGSV_DI void pass_gtq(const BatchMat& g, int r0, int r1, int n, bool final_pass) {
+    if constexpr (kRegStream) {
+      pass_gtq_reg(g, r0, r1, n, final_pass);
+      return;
+    }
     constexpr int kIB = NP / 8, kJB = KP / 8, kBlocks = kIB * kJB;
     constexpr int kPer = (kBlocks + kWarps - 1) / kWarps;
     double acc[kPer][2][2] = {};
@@ -739,7 +961,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       C.cholqr3(tall ? C.ys : C.zb, tall ? rlt : NP, k, tall ? rows : n, tall, tall);
       PROF(9);
       if (tall) {
-        C.pass_gtq(g, r0, r1, n);
+        C.pass_gtq(g, r0, r1, n, hs == last);
         PROF(2);
         C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
         C.trsm(C.zb, NP);  // the deferred L3^-T of Q
