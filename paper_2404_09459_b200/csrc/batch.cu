@@ -609,7 +609,8 @@ struct Chain {
   //      needs no separate substitution sweep. Row j is broadcast by
   //      independent shuffles; the critical path per step is one shuffle,
   //      one rsqrt and one FMA.
-  RGSV_DI void chol(int k, int64_t shift_rows) {
+  //      Returns true when the near-identity route produced the inverse.
+  RGSV_DI bool chol(int k, int64_t shift_rows) {
     constexpr int LD = KP + 1;
     static_assert(KP <= 32, "one lane per row");
 #ifdef RGSV_BATCH_PROFILE
@@ -620,12 +621,12 @@ struct Chain {
 #ifdef RGSV_BATCH_PROFILE
       if (tid == 0) atomicAdd(&g_batch_prof[13], (unsigned long long)(clock64() - _c0));
 #endif
-      return;
+      return true;
     }
     if constexpr (KP == 16) {
       chol16(k, shift_rows);
       __syncthreads();
-      return;
+      return false;
     }
     if (warp == 0) {
 #ifdef RGSV_BATCH_PROFILE
@@ -695,6 +696,7 @@ struct Chain {
 #endif
     }
     __syncthreads();
+    return false;
   }
 
   // ---- the same symmetric Gauss-Jordan for KP = 16 on the whole CTA: thread
@@ -873,15 +875,28 @@ struct Chain {
   //      Q2 and linv holds L3^-1 -- because the only consumer of Q is the
   //      next G^T Q pass: G^T (Q2 L3^-T) = (G^T Q2) L3^-T is applied to the
   //      reduced n x k product instead of the m x k slice.
+  //      The passes stop as soon as one of them (after the shifted first)
+  //      found its Gram within 1e-6 of I: near_identity_inverse is exact to
+  //      O(|E|^3) <= 1e-18 there, so the basis it produces is orthonormal to
+  //      rounding and a further pass could only re-round it.
+  //      side: a block-local scalar (||G||^2 partial) summed over the cluster
+  //      together with the first Gram (one cluster barrier instead of two);
+  //      the total lands in misc[0].
   RGSV_DI void cholqr3(double* buf, int rows, int k, int64_t shift_rows, bool sharded,
-                       bool defer_last = false) {
+                       bool defer_last = false, const double* side = nullptr) {
     constexpr int LD = KP + 1;
+    static_assert(KP * KP + 1 <= Lo::kPart, "Gram + side scalar fit a reduction slot");
     PROF_T0();
     for (int pass = 0; pass < 3; ++pass) {
       gram_partial(buf, rows);
       PROF(4);
       if (sharded) {
-        reduce(KP * KP, [&](int e, double s) { gram[(e / KP) * LD + (e % KP)] = s; });
+        const bool with_side = side != nullptr && pass == 0;
+        if (with_side && tid == 0) slot_ptr()[KP * KP] = *side;
+        reduce(KP * KP + (with_side ? 1 : 0), [&](int e, double s) {
+          if (e < KP * KP) gram[(e / KP) * LD + (e % KP)] = s;
+          else misc[0] = s;
+        });
       } else {
         __syncthreads();
         const double* src = slot_ptr();
@@ -889,11 +904,13 @@ struct Chain {
         __syncthreads();
       }
       PROF(5);
-      chol(k, pass == 0 ? shift_rows : 0);
+      const bool converged = chol(k, pass == 0 ? shift_rows : 0);
       PROF(6);
-      if (defer_last && pass == 2) break;
+      const bool last_pass = pass == 2 || (pass >= 1 && converged);
+      if (defer_last && last_pass) break;
       trsm(buf, rows);
       PROF(7);
+      if (last_pass) break;
     }
   }
 };
@@ -945,20 +962,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
         C.pass_gx(g, r0, r1, n, hs == 0 ? &ss : nullptr);
         __syncthreads();
         PROF(1);
-        if (hs == 0) {  // ||G||_F^2: block partial in fixed order -> cluster sum
+        if (hs == 0) {  // ||G||_F^2: block partial in fixed order; summed over the
+                        // cluster with the first Gram (cholqr3's side scalar)
           double v = warp_sum(ss);
           if (C.lane == 0) C.wred[C.warp * 64] = v;
           __syncthreads();
           if (C.tid == 0) {
             double s = 0.0;
             for (int w = 0; w < kWarps; ++w) s += C.wred[w * 64];
-            C.slot_ptr()[0] = s;
+            C.misc[1] = s;
           }
-          C.reduce(1, [&](int, double s) { C.misc[0] = s; });
+          __syncthreads();
           PROF(8);
         }
       }
-      C.cholqr3(tall ? C.ys : C.zb, tall ? rlt : NP, k, tall ? rows : n, tall, tall);
+      C.cholqr3(tall ? C.ys : C.zb, tall ? rlt : NP, k, tall ? rows : n, tall, tall,
+                hs == 0 ? C.misc + 1 : nullptr);
       PROF(9);
       if (tall) {
         C.pass_gtq(g, r0, r1, n, hs == last);
