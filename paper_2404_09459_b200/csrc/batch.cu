@@ -704,8 +704,8 @@ struct Chain {
   //      Per pivot j it needs the pivot row (A[j][c], X[j][c]), its own row's
   //      column-j entry A[i][j] and d = A[j][j]: every thread publishes its
   //      two entries in a double-buffered shared-memory copy, so one CTA
-  //      barrier per pivot suffices. The j loop is NOT unrolled: the body is
-  //      ~60 instructions that stay in the instruction cache (the unrolled
+  //      barrier per published state suffices. The j loop is NOT unrolled: the
+  //      body is ~100 instructions that stay in the instruction cache (the unrolled
   //      one-warp form was 2500 instructions per call site, executed once per
   //      call, i.e. instruction-fetch bound: 9.5 us per call). Same operations
   //      in the same order per entry as the one-warp form (bitwise equal).
@@ -735,24 +735,46 @@ struct Chain {
       __syncthreads();
     }
     bool bad = false;
+    // Two pivots (j, j + 1) per published state: every thread re-derives what
+    // pivot j does to row j + 1, column j + 1 and d_{j+1} with the very
+    // operations their owner threads perform, so the result equals the
+    // one-pivot-per-barrier sweep bit for bit at half the barriers and
+    // shared-memory round trips (the sweep is a pure latency chain).
 #pragma unroll 1
-    for (int j = 0; j < 16; ++j) {
-      double* pa = pub + (j & 1) * (2 * 16 * LD);
+    for (int j = 0; j < 16; j += 2) {
+      double* pa = pub + ((j >> 1) & 1) * (2 * 16 * LD);
       double* px = pa + 16 * LD;
       pa[i * LD + c] = a;
       px[i * LD + c] = x;
       __syncthreads();
-      const double d = pa[j * LD + j];
-      const double aij = pa[i * LD + j];
-      const double rowa = pa[j * LD + c];
-      const double rowx = px[j * LD + c];
-      bad |= !(d > 0.0) || !isfinite(d);
-      const double r = rsqrt(d);
-      const double ff = (i > j) ? aij * (r * r) : 0.0;
-      const double mul = (i == j) ? r : 1.0;
-      if (c > j) a = fma(-ff, rowa, a) * mul;
-      else x = fma(-ff, rowx, x) * mul;
-      if (c == j) a = (i > j) ? 0.0 : (i == j ? d * r : a);
+      const double d0 = pa[j * LD + j], b10 = pa[(j + 1) * LD + j];
+      const double u01 = pa[j * LD + j + 1], e11 = pa[(j + 1) * LD + j + 1];
+      const double ai0 = pa[i * LD + j], ai1 = pa[i * LD + j + 1];
+      const double ra0 = pa[j * LD + c], ra1 = pa[(j + 1) * LD + c];
+      const double rx0 = px[j * LD + c], rx1 = px[(j + 1) * LD + c];
+      // pivot j
+      bad |= !(d0 > 0.0) || !isfinite(d0);
+      const double r0 = rsqrt(d0);
+      const double rr0 = r0 * r0;
+      const double ff0 = (i > j) ? ai0 * rr0 : 0.0;
+      const double mul0 = (i == j) ? r0 : 1.0;
+      if (c > j) a = fma(-ff0, ra0, a) * mul0;
+      else x = fma(-ff0, rx0, x) * mul0;
+      if (c == j) a = (i > j) ? 0.0 : (i == j ? d0 * r0 : a);
+      // what pivot j did to row j + 1 (multiplier f10, scale 1) and column j + 1
+      const double f10 = b10 * rr0;
+      const double d1 = fma(-f10, u01, e11) * 1.0;
+      const double ra1n = fma(-f10, ra0, ra1) * 1.0;               // used for c > j + 1
+      const double rx1n = (c <= j) ? fma(-f10, rx0, rx1) * 1.0 : rx1;  // c == j + 1: untouched
+      const double ai1n = fma(-ff0, u01, ai1) * 1.0;               // used for i > j + 1
+      // pivot j + 1
+      bad |= !(d1 > 0.0) || !isfinite(d1);
+      const double r1 = rsqrt(d1);
+      const double ff1 = (i > j + 1) ? ai1n * (r1 * r1) : 0.0;
+      const double mul1 = (i == j + 1) ? r1 : 1.0;
+      if (c > j + 1) a = fma(-ff1, ra1n, a) * mul1;
+      else x = fma(-ff1, rx1n, x) * mul1;
+      if (c == j + 1) a = (i > j + 1) ? 0.0 : (i == j + 1 ? d1 * r1 : a);
     }
     if (bad) fail = 1;
     __syncthreads();  // wred (pub) is reused by the callers right after

@@ -11,9 +11,13 @@ from paper_2404_09459_b200.workloads import CONFIGS  # noqa: E402
 
 cfg = CONFIGS["cfg3"]
 B = int(os.environ.get("B", cfg.batch))
-gen = torch.Generator(device="cuda").manual_seed(0)
-g1 = torch.randn((B, cfg.m, cfg.n), generator=gen, device="cuda", dtype=torch.float64)
-g2 = torch.randn((B, cfg.p, cfg.n), generator=gen, device="cuda", dtype=torch.float64)
+if os.environ.get("DATA", "cfg3") == "gauss":  # plain Gaussian matrices (well conditioned)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    g1 = torch.randn((B, cfg.m, cfg.n), generator=gen, device="cuda", dtype=torch.float64)
+    g2 = torch.randn((B, cfg.p, cfg.n), generator=gen, device="cuda", dtype=torch.float64)
+else:  # the bench's cfg3 data (workloads.py recipe: rank-8 signal + 1e-8 noise)
+    import bench
+    g1, g2 = bench.device_batch_pairs(cfg, B, 1000)
 pairs = [(rg.device.DevMatrix(g1[j], cfg.m, cfg.n), rg.device.DevMatrix(g2[j], cfg.p, cfg.n))
          for j in range(B)]
 plan = rg.device.small_batch_plan(B, cfg.n, cfg.k)
