@@ -98,9 +98,16 @@ RGSV_DI void ldg_stream2(double& x, double& y, const double* p) {
 // three passes keep their lines (evict_last), the last one marks them dead
 // (evict_first) so finished matrices do not push live ones out.
 RGSV_DI void ldg_stream2(double& x, double& y, const double* p, uint64_t pol) {
+#ifdef RGSV_BATCH_PLAIN_LDG
+  (void)pol;
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  x = v.x;
+  y = v.y;
+#else
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(x), "=d"(y)
                : "l"(p), "l"(pol));
+#endif
 }
 RGSV_DI uint64_t l2_policy(bool keep) {
   uint64_t pol;
@@ -268,17 +275,44 @@ struct Chain {
   //      (gtq) index inside each group of 8 / 16 columns; both operands use
   //      the same one, and the order of every sum is fixed.
   static constexpr bool kRegStream = (NP == 64 && KP == 16);
-#ifndef RGSV_BATCH_DGX
-#define RGSV_BATCH_DGX 3
-#endif
-#ifndef RGSV_BATCH_DGTQ
-#define RGSV_BATCH_DGTQ 2
-#endif
+
+  // Software pipeline shared by both passes. A warp owns `cnt` blocks, the
+  // first `cntf` of them loadable without predicates (whole rows, n == NP).
+  // ptxas tracks every streaming load of this kernel on ONE scoreboard (the
+  // DMMA chains and the shared-memory loads take the others), so a consumer
+  // that waits for its block waits for every load in flight, and a classic
+  // k-deep register pipeline collapses to depth zero (measured: 2, 3 and 4
+  // deep ran alike, with the warps stalled on the first DMMA of each block,
+  // profiles/r02_batch_chain_*). The order that does overlap under that
+  // constraint: the first DMMAs of block i wait for block i (and thereby for
+  // everything issued so far), THEN the loads of block i + 1 are issued, then
+  // the rest of block i computes without any further wait on the load
+  // scoreboard. Two register buffers; the steady state is one basic block
+  // per pair of blocks (the refill index is clamped, not guarded).
+  // compute(d, i, hook) must call hook() once, after its first DMMAs.
+  template <typename LoadFast, typename LoadSlow, typename Compute>
+  RGSV_DI void pipeline(int cnt, int cntf, LoadFast&& load_fast, LoadSlow&& load_slow,
+                        Compute&& compute) {
+    if (cntf > 0) {
+      load_fast(0, 0);
+      const int pairs = cntf >> 1;
+      for (int gp = 0; gp < pairs; ++gp) {
+        const int i = 2 * gp;
+        compute(0, i, [&] { load_fast(1, i + 1); });
+        compute(1, i + 1, [&] { load_fast(0, min(i + 2, cntf - 1)); });  // clamped re-read
+      }
+      if (cntf & 1) compute(0, cntf - 1, [] {});
+    }
+    for (int i = cntf; i < cnt; ++i) {  // partial blocks / ragged columns: not pipelined
+      load_slow(0, i);
+      compute(0, i, [] {});
+    }
+  }
 
   // Y[8-row block] = G_block X: thread (g, t) loads G[row g][8u + 2t, +1];
   // k-step 2u + h contracts the columns 8u + 2t + h.
   RGSV_DI void pass_gx_reg(const BatchMat& g, int r0, int r1, int n, double* ss) {
-    constexpr int NK = NP / 4, NCB = KP / 8, kDepth = RGSV_BATCH_DGX;
+    constexpr int NK = NP / 4, NCB = KP / 8;
     const int gq = lane >> 2, t = lane & 3;
     double xf[NCB][NK];
 #pragma unroll
@@ -287,113 +321,115 @@ struct Chain {
       for (int sidx = 0; sidx < NK; ++sidx)
         xf[cb][sidx] = xt[(cb * 8 + gq) * GP + 8 * (sidx >> 1) + 2 * t + (sidx & 1)];
     const int nblk = (r1 - r0 + 7) / 8;
+    const int nfull = n == NP ? (r1 - r0) / 8 : 0;
     const int cnt = nblk > warp ? (nblk - warp + kWarps - 1) / kWarps : 0;
-    double a[kDepth][NK];
+    const int cntf = nfull > warp ? (nfull - warp + kWarps - 1) / kWarps : 0;
+    double a[2][NK];
     const uint64_t pol = l2_policy(true);
     const double* gbase = g.g + (int64_t)(r0 + gq) * g.ld + 2 * t;
     const int64_t bstride = 8 * g.ld;
-    auto load = [&](double (&dst)[NK], int i) {
-      const int b = warp + i * kWarps;
-      const double* src = gbase + b * bstride;
-      if (n == NP && r0 + b * 8 + 8 <= r1) {  // whole block, whole rows: no predicates
-#pragma unroll
-        for (int u = 0; u < NP / 8; ++u) ldg_stream2(dst[2 * u], dst[2 * u + 1], src + 8 * u, pol);
-        return;
-      }
-      const int row = r0 + b * 8 + gq;
-      const bool rok = row < r1;
-#pragma unroll
-      for (int u = 0; u < NP / 8; ++u) {
-        const int col = 8 * u + 2 * t;
-        if (rok && col + 1 < n) {
-          ldg_stream2(dst[2 * u], dst[2 * u + 1], src + 8 * u);
-        } else {
-          dst[2 * u] = (rok && col < n) ? ldg_stream1(src + 8 * u) : 0.0;
-          dst[2 * u + 1] = 0.0;
-        }
-      }
-    };
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d)
-      if (d < cnt) load(a[d], d);
     double sq = 0.0;
-    for (int i = 0; i < cnt; i += kDepth) {
+    const bool want_ss = ss != nullptr;
+    pipeline(
+        cnt, cntf,
+        [&](int d, int i) {
+          const double* src = gbase + (warp + i * kWarps) * bstride;
 #pragma unroll
-      for (int d = 0; d < kDepth; ++d) {
-        if (i + d < cnt) {
+          for (int u = 0; u < NP / 8; ++u)
+            ldg_stream2(a[d][2 * u], a[d][2 * u + 1], src + 8 * u, pol);
+        },
+        [&](int d, int i) {
+          const int b = warp + i * kWarps;
+          const double* src = gbase + b * bstride;
+          const bool rok = r0 + b * 8 + gq < r1;
+#pragma unroll
+          for (int u = 0; u < NP / 8; ++u) {
+            const int col = 8 * u + 2 * t;
+            if (rok && col + 1 < n) {
+              ldg_stream2(a[d][2 * u], a[d][2 * u + 1], src + 8 * u);
+            } else {
+              a[d][2 * u] = (rok && col < n) ? ldg_stream1(src + 8 * u) : 0.0;
+              a[d][2 * u + 1] = 0.0;
+            }
+          }
+        },
+        [&](int d, int i, auto&& hook) {
           double c[NCB][2][2] = {};
 #pragma unroll
-          for (int sidx = 0; sidx < NK; ++sidx)
+          for (int cb = 0; cb < NCB; ++cb) dmma(c[cb][0], a[d][0], xf[cb][0]);
+          hook();  // the next block's loads, behind the wait for this one
+#pragma unroll
+          for (int sidx = 1; sidx < NK; ++sidx)
 #pragma unroll
             for (int cb = 0; cb < NCB; ++cb) dmma(c[cb][sidx & 1], a[d][sidx], xf[cb][sidx]);
-          if (ss) {
+          if (want_ss) {
 #pragma unroll
             for (int sidx = 0; sidx < NK; ++sidx) sq = fma(a[d][sidx], a[d][sidx], sq);
           }
-          const int r = (warp + (i + d) * kWarps) * 8 + gq;
+          const int r = (warp + i * kWarps) * 8 + gq;
 #pragma unroll
           for (int cb = 0; cb < NCB; ++cb) {
             const int col = cb * 8 + 2 * t;
             ys[yx<KP>(r, col)] = c[cb][0][0] + c[cb][1][0];
             ys[yx<KP>(r, col + 1)] = c[cb][0][1] + c[cb][1][1];
           }
-          if (i + d + kDepth < cnt) load(a[d], i + d + kDepth);
-        }
-      }
-    }
+        });
     if (ss) *ss += sq;
   }
 
   // part = G^T Y over this CTA's rows: thread (g, t) loads G[row t][16v + 2g,
-  // +1]; output block 2v + h holds the G columns 16v + 2g + h. Every warp
-  // accumulates the whole NP x KP product over its own rows; the 8 warp
+  // +1]; output block 2v + h holds the G columns 16v + 2g + h. Warps work in
+  // pairs: pair p = warp / 2 owns the 8-row blocks p, p + 4, ... and each of
+  // its two warps takes one half of the columns (its own 2 x 128-byte segments
+  // of every row), so a block costs a warp 16 registers; every warp
+  // accumulates its NP/2 x KP half over the pair's rows, and the four pair
   // partials are folded in a fixed order through the (idle) ring memory.
   RGSV_DI void pass_gtq_reg(const BatchMat& g, int r0, int r1, int n, bool final_pass) {
-    constexpr int NV = NP / 16, NJB = KP / 8, SP = KP + 4, kDepth = RGSV_BATCH_DGTQ;  // SP: conflict-free 16 B stores
-    static_assert(4 * NP * SP <= Lo::kG, "warp partials fit the idle ring");
+    constexpr int NV = NP / 32, NJB = KP / 8, SP = KP + 4;
+    constexpr int kPairs = kWarps / 2;
+    static_assert(kPairs * NP * SP <= Lo::kG, "pair partials fit the idle ring");
     const int gq = lane >> 2, t = lane & 3;
+    const int pr = warp >> 1, c0 = (warp & 1) * (NP / 2);  // this warp's column half
     double acc[2 * NV][NJB][2] = {};
     const int nblk = (r1 - r0 + 7) / 8;
-    const int cnt = nblk > warp ? (nblk - warp + kWarps - 1) / kWarps : 0;
-    double a[kDepth][2][NV][2];
+    const int nfull = n == NP ? (r1 - r0) / 8 : 0;
+    const int cnt = nblk > pr ? (nblk - pr + kPairs - 1) / kPairs : 0;
+    const int cntf = nfull > pr ? (nfull - pr + kPairs - 1) / kPairs : 0;
+    double a[2][2][NV][2];
     const uint64_t pol = l2_policy(!final_pass);
-    const double* gbase = g.g + (int64_t)(r0 + t) * g.ld + 2 * gq;
+    const double* gbase = g.g + (int64_t)(r0 + t) * g.ld + c0 + 2 * gq;
     const int64_t bstride = 8 * g.ld, hstride = 4 * g.ld;
-    auto load = [&](double (&dst)[2][NV][2], int i) {
-      const int b = warp + i * kWarps;
-      if (n == NP && r0 + b * 8 + 8 <= r1) {  // whole block, whole rows: no predicates
+    pipeline(
+        cnt, cntf,
+        [&](int d, int i) {
+          const double* src = gbase + (pr + i * kPairs) * bstride;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int v = 0; v < NV; ++v)
-            ldg_stream2(dst[h][v][0], dst[h][v][1], gbase + b * bstride + h * hstride + 16 * v, pol);
-        return;
-      }
+            for (int v = 0; v < NV; ++v)
+              ldg_stream2(a[d][h][v][0], a[d][h][v][1], src + h * hstride + 16 * v, pol);
+        },
+        [&](int d, int i) {
+          const int b = pr + i * kPairs;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int row = r0 + b * 8 + 4 * h + t;
-        const bool rok = row < r1;
-        const double* src = g.g + (int64_t)row * g.ld + 2 * gq;
+          for (int h = 0; h < 2; ++h) {
+            const int row = r0 + b * 8 + 4 * h + t;
+            const bool rok = row < r1;
+            const double* src = g.g + (int64_t)row * g.ld + c0 + 2 * gq;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int col = 16 * v + 2 * gq;
-          if (rok && col + 1 < n) {
-            ldg_stream2(dst[h][v][0], dst[h][v][1], src + 16 * v);
-          } else {
-            dst[h][v][0] = (rok && col < n) ? ldg_stream1(src + 16 * v) : 0.0;
-            dst[h][v][1] = 0.0;
+            for (int v = 0; v < NV; ++v) {
+              const int col = c0 + 16 * v + 2 * gq;
+              if (rok && col + 1 < n) {
+                ldg_stream2(a[d][h][v][0], a[d][h][v][1], src + 16 * v);
+              } else {
+                a[d][h][v][0] = (rok && col < n) ? ldg_stream1(src + 16 * v) : 0.0;
+                a[d][h][v][1] = 0.0;
+              }
+            }
           }
-        }
-      }
-    };
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d)
-      if (d < cnt) load(a[d], d);
-    for (int i = 0; i < cnt; i += kDepth) {
-#pragma unroll
-      for (int d = 0; d < kDepth; ++d) {
-        if (i + d < cnt) {
-          const int rl0 = (warp + (i + d) * kWarps) * 8;
+        },
+        [&](int d, int i, auto&& hook) {
+          const int rl0 = (pr + i * kPairs) * 8;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             double bf[NJB];
@@ -402,43 +438,32 @@ struct Chain {
 #pragma unroll
             for (int v = 0; v < NV; ++v)
 #pragma unroll
-              for (int e = 0; e < 2; ++e)
+              for (int e = 0; e < 2; ++e) {
 #pragma unroll
                 for (int jb = 0; jb < NJB; ++jb) dmma(acc[2 * v + e][jb], a[d][h][v][e], bf[jb]);
+                if (h == 0 && v == 0 && e == 0) hook();  // next loads behind this block's wait
+              }
           }
-          if (i + d + kDepth < cnt) load(a[d], i + d + kDepth);
-        }
-      }
-    }
-    // fold the warp partials: ((w0 + w4) + (w1 + w5)) + ((w2 + w6) + (w3 + w7))
-    double* scr = gst + (warp & 3) * (NP * SP);
+        });
+    // pair p writes its two column halves into scratch slot p; fixed-order fold
+    double* scr = gst + pr * (NP * SP);
     __syncthreads();  // the ring memory (zb / wred) is no longer read
 #pragma unroll
-    for (int ph = 0; ph < 2; ++ph) {
-      if ((warp >> 2) == ph) {
+    for (int v = 0; v < NV; ++v)
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-#pragma unroll
-            for (int jb = 0; jb < NJB; ++jb) {
-              double2* q = reinterpret_cast<double2*>(scr + (16 * v + 2 * gq + e) * SP + jb * 8 +
-                                                      2 * t);
-              double2 val = make_double2(acc[2 * v + e][jb][0], acc[2 * v + e][jb][1]);
-              if (ph == 1) {
-                const double2 o = *q;
-                val.x = o.x + val.x;
-                val.y = o.y + val.y;
-              }
-              *q = val;
-            }
-      }
-      __syncthreads();
-    }
+        for (int jb = 0; jb < NJB; ++jb)
+          *reinterpret_cast<double2*>(scr + (c0 + 16 * v + 2 * gq + e) * SP + jb * 8 + 2 * t) =
+              make_double2(acc[2 * v + e][jb][0], acc[2 * v + e][jb][1]);
+    __syncthreads();
     double* dst = slot_ptr();
     for (int e = tid; e < NP * KP; e += kThreads) {
       const int o = (e / KP) * SP + (e % KP);
-      dst[e] = (gst[o] + gst[NP * SP + o]) + (gst[2 * NP * SP + o] + gst[3 * NP * SP + o]);
+      double sum = gst[o];
+#pragma unroll
+      for (int q = 1; q < kPairs; ++q) sum += gst[q * NP * SP + o];
+      dst[e] = sum;
     }
   }
 

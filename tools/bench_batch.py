@@ -18,8 +18,9 @@ if os.environ.get("DATA", "cfg3") == "gauss":  # plain Gaussian matrices (well c
 else:  # the bench's cfg3 data (workloads.py recipe: rank-8 signal + 1e-8 noise)
     import bench
     g1, g2 = bench.device_batch_pairs(cfg, B, 1000)
-pairs = [(rg.device.DevMatrix(g1[j], cfg.m, cfg.n), rg.device.DevMatrix(g2[j], cfg.p, cfg.n))
-         for j in range(B)]
+ALIAS = int(os.environ.get("ALIAS", 0))  # >0: every pair aliases one of ALIAS pairs (L2-resident G)
+pairs = [(rg.device.DevMatrix(g1[j % ALIAS if ALIAS else j], cfg.m, cfg.n),
+          rg.device.DevMatrix(g2[j % ALIAS if ALIAS else j], cfg.p, cfg.n)) for j in range(B)]
 plan = rg.device.small_batch_plan(B, cfg.n, cfg.k)
 plan.set_pairs(pairs)
 plan.set_seeds([2 * j for j in range(B)])
