@@ -984,7 +984,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       const int i = e / NP, j = e % NP;
       C.xt[i * C.GP + j] = (i < k && j < n) ? om[(int64_t)i * A.ldo + j] : 0.0;
     }
-    for (int e = C.tid; e < A.yrows * KP; e += kThreads) C.ys[e] = 0.0;
+    // Y rows the passes never write must read as zero in the Grams / TRSMs
+    // (they run over rlt rows): the register passes write whole 8-row blocks,
+    // so only the rows behind the last block are cleared; the ring passes
+    // write every row of their 32-row tiles themselves (zero-filled copies).
+    if constexpr (Chain<NP, KP, CS>::kRegStream) {
+      for (int e = ((rl + 7) / 8) * 8 * KP + C.tid; e < rlt * KP; e += kThreads) C.ys[e] = 0.0;
+    } else {
+      for (int e = C.tid; e < A.yrows * KP; e += kThreads) C.ys[e] = 0.0;
+    }
     __syncthreads();
     // One textual instance of every phase (the chain used to inline three
     // cholqr3 and two bodies of each pass: 315 KB of code run once per
