@@ -1,4 +1,4 @@
-# HEAD baseline after container re-creation: full GPU suite, bench lines of every config
+# baseline at the start of the last session: full GPU suite, bench lines of every config
 mkdir -p gpurun_out/r02z
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02z/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02z/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/r02z/bench_cfg2.json 2> gpurun_out/r02z/bench_cfg2.err
