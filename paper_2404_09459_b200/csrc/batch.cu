@@ -161,12 +161,22 @@ RGSV_DI int gx_idx(int r, int c) {
 
 template <int NP, int KP>
 struct Layout {
+  // NP = 64, KP = 16 (the cfg3 shape) streams G through registers (Chain's
+  // pass_*_reg): no ring, so the region only holds zb + wred, the two fold
+  // slots of pass_gtq_reg and the folded Z / B partial the cluster reduces
+  // from; the reduction slots then only carry a Gram. The smaller footprint
+  // lets a 4000-row matrix run on a 3-CTA cluster.
+  static constexpr bool kRegStream = (NP == 64 && KP == 16);
+  static constexpr int SP = KP + 4;                 // fold-slot pitch (conflict-free 16 B stores)
+  static constexpr int kFold = 2 * NP * SP;         // two fold slots (alias zb + wred)
   static constexpr int GP = NP + 4;                 // X^T pitch (doubles)
-  static constexpr int kG = kStages * kTR * NP;     // G ring (also holds zb + wred between passes)
+  static constexpr int kG = kRegStream ? kFold + NP * KP
+                                       : kStages * kTR * NP;  // G ring / scratch region
   static constexpr int kX = KP * GP;                // X^T (KP x NP)
-  static constexpr int kPart = NP * KP;             // one reduction slot
+  static constexpr int kPart = kRegStream ? KP * KP + 16 : NP * KP;  // one reduction slot
   static constexpr int kSmall = KP * (KP + 1);      // Gram / L / L^-1
-  static_assert(NP * KP + kWarps * 3 * 64 <= kG, "zb + wred must fit the idle G ring");
+  static_assert(NP * KP + kWarps * 3 * 64 <= (kRegStream ? kFold : kG),
+                "zb + wred must fit the idle region");
   static size_t bytes(int yrows) {
     return sizeof(double) * ((size_t)yrows * KP + kG + kX + 2 * kPart + 3 * kSmall + 64);
   }
@@ -231,6 +241,34 @@ struct Chain {
     __syncthreads();
   }
 
+  // ---- the same from an explicit source that is rewritten only after later
+  //      cluster barriers (the folded Z / B partial of pass_gtq_reg)
+  template <typename F>
+  RGSV_DI void reduce_from(const double* src, int cnt, F&& store) {
+    __syncthreads();
+    cluster_barrier();
+    for (int e = tid; e < cnt; e += kThreads) {
+      double v[CS];
+#pragma unroll
+      for (int r = 0; r < CS; ++r) v[r] = ld_dsmem(src + e, r);
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < CS; ++r) s += v[r];
+      store(e, s);
+    }
+    __syncthreads();
+  }
+  // the n x k partial of this CTA's last pass_gtq
+  RGSV_DI const double* gtq_partial() {
+    if constexpr (kRegStream) return gst + Lo::kFold;
+    else return slot_ptr();
+  }
+  template <typename F>
+  RGSV_DI void reduce_gtq(F&& store) {
+    if constexpr (kRegStream) reduce_from(gst + Lo::kFold, NP * KP, store);
+    else reduce(NP * KP, store);
+  }
+
   // ---- stream this CTA's G rows [r0, r1) through the ring, tile by tile
   RGSV_DI void issue_tile(const BatchMat& g, int r0, int r1, int t, int n) {
     double* dst = gst + (t % kStages) * kTR * NP;
@@ -274,7 +312,7 @@ struct Chain {
   //      16-byte loads fix a permutation of the contraction (gx) / output row
   //      (gtq) index inside each group of 8 / 16 columns; both operands use
   //      the same one, and the order of every sum is fixed.
-  static constexpr bool kRegStream = (NP == 64 && KP == 16);
+  static constexpr bool kRegStream = Lo::kRegStream;
 
   // Software pipeline shared by both passes. A warp owns `cnt` blocks, the
   // first `cntf` of them loadable without predicates (whole rows, n == NP).
@@ -385,9 +423,9 @@ struct Chain {
   // accumulates its NP/2 x KP half over the pair's rows, and the four pair
   // partials are folded in a fixed order through the (idle) ring memory.
   RGSV_DI void pass_gtq_reg(const BatchMat& g, int r0, int r1, int n, bool final_pass) {
-    constexpr int NV = NP / 32, NJB = KP / 8, SP = KP + 4;
+    constexpr int NV = NP / 32, NJB = KP / 8, SP = Lo::SP;
     constexpr int kPairs = kWarps / 2;
-    static_assert(kPairs * NP * SP <= Lo::kG, "pair partials fit the idle ring");
+    static_assert(kPairs == 4, "two fold slots, two phases");
     const int gq = lane >> 2, t = lane & 3;
     const int pr = warp >> 1, c0 = (warp & 1) * (NP / 2);  // this warp's column half
     double acc[2 * NV][NJB][2] = {};
@@ -445,25 +483,38 @@ struct Chain {
               }
           }
         });
-    // pair p writes its two column halves into scratch slot p; fixed-order fold
-    double* scr = gst + pr * (NP * SP);
-    __syncthreads();  // the ring memory (zb / wred) is no longer read
+    // fixed-order fold through two slots: pairs 0, 1 store, pairs 2, 3 add
+    // theirs, then (p0 + p2) + (p1 + p3) lands in the region the cluster
+    // reduction reads (rewritten only by the next pass_gtq, several cluster
+    // barriers later)
+    double* scr = gst + (pr & 1) * (NP * SP);
+    __syncthreads();  // zb / wred (aliased by the fold slots) are no longer read
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+    for (int ph = 0; ph < kPairs / 2; ++ph) {
+      if ((pr >> 1) == ph) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+        for (int v = 0; v < NV; ++v)
 #pragma unroll
-        for (int jb = 0; jb < NJB; ++jb)
-          *reinterpret_cast<double2*>(scr + (c0 + 16 * v + 2 * gq + e) * SP + jb * 8 + 2 * t) =
-              make_double2(acc[2 * v + e][jb][0], acc[2 * v + e][jb][1]);
-    __syncthreads();
-    double* dst = slot_ptr();
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int jb = 0; jb < NJB; ++jb) {
+              double2* q = reinterpret_cast<double2*>(scr + (c0 + 16 * v + 2 * gq + e) * SP +
+                                                      jb * 8 + 2 * t);
+              double2 val = make_double2(acc[2 * v + e][jb][0], acc[2 * v + e][jb][1]);
+              if (ph > 0) {
+                const double2 o = *q;
+                val.x = o.x + val.x;
+                val.y = o.y + val.y;
+              }
+              *q = val;
+            }
+      }
+      __syncthreads();
+    }
+    double* dst = gst + Lo::kFold;
     for (int e = tid; e < NP * KP; e += kThreads) {
       const int o = (e / KP) * SP + (e % KP);
-      double sum = gst[o];
-#pragma unroll
-      for (int q = 1; q < kPairs; ++q) sum += gst[q * NP * SP + o];
-      dst[e] = sum;
+      dst[e] = gst[o] + gst[NP * SP + o];
     }
   }
 
@@ -1037,7 +1088,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
       if (tall) {
         C.pass_gtq(g, r0, r1, n, hs == last);
         PROF(2);
-        C.reduce(NP * KP, [&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
+        C.reduce_gtq([&](int e, double s) { C.zb[yx<KP>(e / KP, e % KP)] = s; });
         C.trsm(C.zb, NP);  // the deferred L3^-T of Q
         PROF(10);
         if (hs == last) break;
@@ -1093,8 +1144,8 @@ int launch_chain_t(const ChainArgs& a, cudaStream_t st) {
   cfg.numAttrs = 1;
   // persistent clusters: exactly as many as can be co-resident, otherwise the
   // clusters that do not fit would run their whole matrix list afterwards
-  static int resident[4] = {0, 0, 0, 0};
-  int& clusters_max = resident[CS == 1 ? 0 : CS == 2 ? 1 : CS == 4 ? 2 : 3];
+  static int resident[9] = {};
+  int& clusters_max = resident[CS];
   if (clusters_max == 0) {
     cfg.gridDim = dim3(kSMs / CS * CS, 1, 1);
     if (cudaOccupancyMaxActiveClusters(&clusters_max, (void*)kern, &cfg) != cudaSuccess ||
@@ -1114,6 +1165,7 @@ int launch_chain_np(const ChainArgs& a, int cs, cudaStream_t st) {
   switch (cs) {
     case 1: return launch_chain_t<NP, KP, 1>(a, st);
     case 2: return launch_chain_t<NP, KP, 2>(a, st);
+    case 3: return launch_chain_t<NP, KP, 3>(a, st);
     case 4: return launch_chain_t<NP, KP, 4>(a, st);
     case 8: return launch_chain_t<NP, KP, 8>(a, st);
   }
@@ -1133,9 +1185,13 @@ int batch_chain_plan(int max_rows, int n, int k, int* cs_out, int* yrows_out) {
   static const int cs_min = [] {
     const char* e = getenv("RGSV_BATCH_CS");
     const int v = e ? atoi(e) : 1;
-    return (v == 2 || v == 4 || v == 8) ? v : 1;
+    return (v == 2 || v == 3 || v == 4 || v == 8) ? v : 1;
   }();
-  for (int cs = cs_min; cs <= 8; cs *= 2) {
+  // 3-CTA clusters pack the GPCs better than 4 (48 x 3 vs 33 x 4 SMs busy)
+  // and spread a matrix's serial phases over fewer SMs
+  static const int sizes[] = {1, 2, 3, 4, 8};
+  for (int cs : sizes) {
+    if (cs < cs_min) continue;
     const int rpc = (max_rows + cs - 1) / cs;
     const int yrows = (rpc + kTR - 1) / kTR * kTR;
     size_t bytes;

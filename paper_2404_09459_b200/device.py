@@ -636,7 +636,13 @@ class SmallBatchPlan:
     def set_seeds(self, seeds) -> None:
         """Omega stream seeds: G1_j from seeds[j], G2_j from seeds[j] + 1
         (engine.py:252-253), reduced mod 2^64 like rangefinder.py:101."""
-        sd = np.fromiter((int(x) & SEED_MASK for x in seeds), dtype=np.uint64, count=len(seeds))
+        try:  # one vectorized conversion when every seed fits int64 (the usual case)
+            sd = np.asarray(seeds, dtype=np.int64).astype(np.uint64)  # two's complement = mod 2^64
+            if sd.ndim != 1:
+                raise TypeError
+        except (OverflowError, TypeError, ValueError):
+            sd = np.fromiter((int(x) & SEED_MASK for x in seeds), dtype=np.uint64,
+                             count=len(seeds))
         words = np.empty(2 * len(sd), dtype=np.uint64)
         words[0::2] = sd
         words[1::2] = sd + np.uint64(1)  # wraps mod 2^64
