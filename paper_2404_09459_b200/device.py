@@ -614,23 +614,31 @@ class SmallBatchPlan:
         self.desc = torch.zeros(2 * B * _DESC.itemsize, dtype=torch.uint8, device="cuda")
         self.seeds = torch.zeros(2 * B, dtype=torch.int64, device="cuda")
         self._desc_key = None
+        self._pairs_key = None
         self._seed_key = None
 
-    def set_pairs(self, pairs) -> int:
+    def set_pairs(self, pairs, key=None) -> int:
         """Descriptors {G1_j, G2_j} of the (resident) pairs; returns max rows.
         Cached on the identity of the matrix objects (kept referenced here so
-        the identities stay valid while cached)."""
+        the identities stay valid while cached). `key`: an identity key the
+        caller already holds for this very sequence (engine._batch_scan's
+        tuple of pair ids) -- a hit then costs one tuple comparison instead of
+        rebuilding the 2B-entry matrix list."""
+        if key is not None and key == self._pairs_key:
+            return self.max_rows
         mats = [g for pair in pairs for g in pair]
-        key = tuple(map(id, mats))
-        if key != self._desc_key:
+        mkey = tuple(map(id, mats))
+        if mkey != self._desc_key:
             arr = np.zeros(len(mats), dtype=_DESC)
             arr["g"] = [g.t.data_ptr() for g in mats]
             arr["ld"] = [g.ld for g in mats]
             arr["rows"] = [g.rows for g in mats]
             self.desc.copy_(torch.from_numpy(arr.view(np.uint8)))
-            self._desc_key = key
+            self._desc_key = mkey
             self._desc_refs = mats
             self.max_rows = int(arr["rows"].max())
+        self._pairs_key = key
+        self._pairs_refs = pairs if key is not None else None  # keeps the keyed ids valid
         return self.max_rows
 
     def set_seeds(self, seeds) -> None:
@@ -672,8 +680,8 @@ class SmallBatchPlan:
         torch.cuda.current_stream().synchronize()
         return fh.numpy(), ih.numpy()
 
-    def run(self, pairs, seeds, q_iters: int, classify_tol: float):
-        self.set_pairs(pairs)
+    def run(self, pairs, seeds, q_iters: int, classify_tol: float, key=None):
+        self.set_pairs(pairs, key)
         self.set_seeds(seeds)
         self.launch(q_iters, classify_tol)
         return self.fetch()

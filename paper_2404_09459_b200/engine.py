@@ -624,13 +624,26 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
     return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]
 
 
+class _PairMats:
+    """(g1, g2) of every pair, built only if the plan's descriptor cache misses."""
+
+    def __init__(self, pairs):
+        self.pairs = pairs
+
+    def __iter__(self):
+        return ((pr.g1, pr.g2) for pr in self.pairs)
+
+
 def _small_batch_runs(pairs, opts: GsvOptions, seeds, k: int):
     """Many small pairs through rgsv_batch_gsvd (one fused chain launch for
     every matrix, one small-GSVD launch for every pair)."""
     n = pairs[0].n
     plan = _dev.small_batch_plan(len(pairs), n, k)
-    fh, ih = plan.run([(pr.g1, pr.g2) for pr in pairs], seeds, opts.extraction.power_iters,
-                      opts.classify_tol)
+    # run_device_batch scanned exactly this sequence just before: its identity
+    # key (ids of the frozen pairs, kept alive by the scan cache) names it
+    key = _BATCH_SCAN[0] if len(_BATCH_SCAN[0] or ()) == len(pairs) else None
+    fh, ih = plan.run(_PairMats(pairs), seeds, opts.extraction.power_iters, opts.classify_tol,
+                      key=key)
     return SmallBatchRuns(fh, ih, plan, opts)
 
 

@@ -48,9 +48,10 @@ names = {0: "setup (Omega load, Y zero)", 1: "G X passes", 2: "G^T Q passes", 4:
          12: "tail (B write)"}
 tot = sum(buf[i] for i in names)
 nm = 2 * B
+CS = int(os.environ.get("CS", 3))  # CTAs per cluster of the launched kernel (cfg3: 3)
 for i, nmv in names.items():
-    print(f"{nmv:28s} {buf[i] / tot * 100:5.1f}%  {buf[i] / nm / 4 / 1.9e3:8.2f} us/matrix/CTA")
-print(f"total {tot / nm / 4 / 1.9e3:.1f} us per matrix-chain per CTA (clock ~1.9 GHz)")
+    print(f"{nmv:28s} {buf[i] / tot * 100:5.1f}%  {buf[i] / nm / CS / 1.9e3:8.2f} us/matrix/CTA")
+print(f"total {tot / nm / CS / 1.9e3:.1f} us per matrix-chain per CTA (clock ~1.9 GHz)")
 print(f"chol calls {buf[15]}, near-identity fast path {buf[14]} "
       f"({buf[13] / max(buf[14], 1) / 1.9e3:.2f} us each incl. the check); "
       f"all chol phases {buf[6] / max(buf[15], 1) / 1.9e3:.2f} us per call")
