@@ -314,6 +314,9 @@ struct Chain {
   //      the same one, and the order of every sum is fixed.
   static constexpr bool kRegStream = Lo::kRegStream;
 
+#ifndef RGSV_BATCH_PREFETCH
+#define RGSV_BATCH_PREFETCH 6
+#endif
   // Software pipeline shared by both passes. A warp owns `cnt` blocks, the
   // first `cntf` of them loadable without predicates (whole rows, n == NP).
   // ptxas tracks every streaming load of this kernel on ONE scoreboard (the
@@ -368,10 +371,19 @@ struct Chain {
     const int64_t bstride = 8 * g.ld;
     double sq = 0.0;
     const bool want_ss = ss != nullptr;
+    // The sketch pass is the one that reads G from HBM: an L2 prefetch (no
+    // destination register, hence no scoreboard) runs kPrefetch blocks ahead
+    // of the loads, one 128-byte line per lane and block, so the loads find
+    // their lines in L2 like the three later passes do.
+    constexpr int kPrefetch = RGSV_BATCH_PREFETCH;
+    const double* pbase = g.g + (int64_t)(r0 + (lane >> 2)) * g.ld + (lane & 3) * 16;
     pipeline(
         cnt, cntf,
         [&](int d, int i) {
           const double* src = gbase + (warp + i * kWarps) * bstride;
+          if (kPrefetch > 0 && want_ss && i + kPrefetch < cntf)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pbase + (warp + (i + kPrefetch) * kWarps) *
+                                                                      bstride));
 #pragma unroll
           for (int u = 0; u < NP / 8; ++u)
             ldg_stream2(a[d][2 * u], a[d][2 * u + 1], src + 8 * u, pol);
@@ -1067,7 +1079,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
         }
         C.pass_gx(g, r0, r1, n, hs == 0 ? &ss : nullptr);
         __syncthreads();
-        PROF(1);
+        PROF(hs == 0 ? 1 : 3);  // 1: the sketch pass (G from HBM), 3: later G X passes (L2)
         if (hs == 0) {  // ||G||_F^2: block partial in fixed order; summed over the
                         // cluster with the first Gram (cholqr3's side scalar)
           double v = warp_sum(ss);

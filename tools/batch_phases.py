@@ -43,7 +43,7 @@ L.rgsv_debug_batch_profile(buf, 1)
 plan.launch(cfg.q, 1e-10)
 torch.cuda.synchronize()
 rg._native.check(L.rgsv_debug_batch_profile(buf, 0), "profile")
-names = {0: "setup (Omega load, Y zero)", 1: "G X passes", 2: "G^T Q passes", 4: "gram",
+names = {0: "setup (Omega load, Y zero)", 1: "G X sketch pass (HBM)", 3: "G X later passes", 2: "G^T Q passes", 4: "gram",
          5: "gram reduce", 6: "chol", 7: "trsm", 8: "|G|^2 reduce", 10: "Z/B reduce",
          12: "tail (B write)"}
 tot = sum(buf[i] for i in names)
