@@ -4,10 +4,14 @@
 // One thread-block CLUSTER per matrix G (m x n): the cluster's CS CTAs split
 // G's rows, and each CTA keeps its slice of the sketch Y / basis Q in SHARED
 // MEMORY for the whole chain, so shifted CholeskyQR3 (Gram, Cholesky, TRSM)
-// never touches HBM. G is streamed through cp.async tiles (32 rows x n) into
-// FP64 DMMA (mma.sync.m8n8k4) four times per chain (sketch, G^T Q, G Q^,
-// projection); with only ~148/CS matrices in flight the re-reads come from
-// L2. The k x k Gram and n x k partial products are reduced across the
+// never touches HBM. G is streamed into FP64 DMMA (mma.sync.m8n8k4) four
+// times per chain (sketch, G^T Q, G Q^, projection); with only ~148/CS
+// matrices in flight the re-reads come from L2. For the cfg3 shape (n <= 64,
+// k <= 16) G goes from global memory straight into DMMA fragments (16-byte
+// no-allocate loads, two register buffers per warp, no CTA barrier inside a
+// pass; Chain::pass_*_reg) and a 4000-row matrix runs on a 3-CTA cluster;
+// the wider shapes stage 32-row tiles through a cp.async ring. The k x k Gram
+// and n x k partial products are reduced across the
 // cluster through distributed shared memory (mapa + ld.shared::cluster) in a
 // fixed CTA order, so every CTA holds bit-identical small matrices and the
 // result does not depend on scheduling. Per matrix the chain is the same
@@ -98,16 +102,9 @@ RGSV_DI void ldg_stream2(double& x, double& y, const double* p) {
 // three passes keep their lines (evict_last), the last one marks them dead
 // (evict_first) so finished matrices do not push live ones out.
 RGSV_DI void ldg_stream2(double& x, double& y, const double* p, uint64_t pol) {
-#ifdef RGSV_BATCH_PLAIN_LDG
-  (void)pol;
-  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
-  x = v.x;
-  y = v.y;
-#else
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(x), "=d"(y)
                : "l"(p), "l"(pol));
-#endif
 }
 RGSV_DI uint64_t l2_policy(bool keep) {
   uint64_t pol;
@@ -307,8 +304,9 @@ struct Chain {
   //      from global memory (L2 after the first pass) straight into DMMA
   //      fragments, with no shared-memory ring and no CTA barrier inside the
   //      pass: warp w owns the 8-row blocks w, w + 8, ... of the slice and
-  //      keeps kDepth blocks (4 KB each) in flight in registers, ~64-96 KB per
-  //      SM against the ring's 32 KB, which was latency bound at 14 B/clk/SM.
+  //      double-buffers them (4 KB each) in registers (see pipeline()); the
+  //      ring it replaces was latency bound at 14 B/clk/SM with a CTA barrier
+  //      per 32-row tile.
   //      16-byte loads fix a permutation of the contraction (gx) / output row
   //      (gtq) index inside each group of 8 / 16 columns; both operands use
   //      the same one, and the order of every sum is fixed.

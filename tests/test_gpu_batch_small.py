@@ -65,6 +65,39 @@ def test_batch_matches_single_and_oracle(rg, B, m, p):
             assert abs(e - eo) <= 1e-12 * eo
 
 
+@pytest.mark.parametrize("n,k,q,m,p", [(50, 12, 1, 1003, 700),    # <64,16>: ragged columns (n < 64)
+                                       (63, 16, 2, 2500, 1900),   # odd n, two power iterations
+                                       (64, 16, 0, 2001, 1333),   # q = 0, partial last blocks
+                                       (100, 16, 1, 1500, 900),   # <128,16> ring instantiation
+                                       (128, 16, 1, 900, 1100),   # <128,16>, full width
+                                       (40, 20, 1, 600, 450)])    # <64,32>
+def test_batch_other_shapes_match_single_and_oracle(rg, n, k, q, m, p):
+    """Every kernel instantiation behind rgsv_batch_gsvd (register-streamed
+    <64,16> incl. its predicated loads for n < 64 and partial row blocks, and
+    the ring-staged <64,32> and <128,16>) against the single-pair
+    pipeline and the oracle, on ill-conditioned cfg3-structured pairs."""
+    import dataclasses
+
+    cfg = dataclasses.replace(CONFIGS["cfg3"], n=n, k=k, q=q, s=min(8, k // 2), shared=min(4, k // 4))
+    hosts, pairs, seeds = _pairs(rg, cfg, 3, m, p)
+    assert rg.device.small_batch_fits(max(m, p), n, k, k)
+    opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(k, 0, q))
+    runs = rg.engine.run_device_batch(pairs, opts, seeds)
+    for j, (run, (g1, g2)) in enumerate(zip(runs, hosts)):
+        o = orc.run_pipeline(g1, g2, k=k, q=q, seed=seeds[j])
+        assert np.array_equal(run.alphas, o.alphas) and (run.r, run.s) == (o.r, o.s)
+        for basis, ob in ((run.basis1, o.basis1), (run.basis2, o.basis2)):
+            h, ho = basis.residual_history, ob.residual_history
+            assert abs(h[0] - ho[0]) <= 1e-13 * ho[0]
+            e, eo = h[0] ** 2 - h[1] ** 2, ho[0] ** 2 - ho[1] ** 2
+            assert abs(e - eo) <= 1e-12 * eo
+        single = rg.engine.run_device_pipeline(
+            pairs[j], rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(k, seeds[j], q)))
+        assert np.array_equal(run.alphas, single.alphas)
+        for a, b in ((run.theta, single.theta), (run.p1, single.p1), (run.p2, single.p2)):
+            assert np.max(np.abs(a - b)) <= 1e-12
+
+
 def test_batch_projections_match_oracle_rows(rg):
     cfg = CONFIGS["cfg3"]
     B = 4
