@@ -312,6 +312,9 @@ struct Chain {
   //      the same one, and the order of every sum is fixed.
   static constexpr bool kRegStream = Lo::kRegStream;
 
+#ifndef RGSV_BATCH_GX_CHAINS
+#define RGSV_BATCH_GX_CHAINS 4  // DMMA accumulator chains per block in pass_gx_reg (2 or 4)
+#endif
 #ifndef RGSV_BATCH_PREFETCH
 #define RGSV_BATCH_PREFETCH 6
 #endif
@@ -409,7 +412,8 @@ struct Chain {
 #pragma unroll
           for (int sidx = 1; sidx < NK; ++sidx)
 #pragma unroll
-            for (int cb = 0; cb < NCB; ++cb) dmma(c[cb][sidx & 1], a[d][sidx], xf[cb][sidx]);
+            for (int cb = 0; cb < NCB; ++cb)
+              dmma(c[cb][(sidx & 1) * (RGSV_BATCH_GX_CHAINS / 4)], a[d][sidx], xf[cb][sidx]);
           if (want_ss) {
 #pragma unroll
             for (int sidx = 0; sidx < NK; ++sidx) sq = fma(a[d][sidx], a[d][sidx], sq);
