@@ -81,6 +81,13 @@ RGSV_DI double ld_dsmem(const double* local, uint32_t rank) {
   asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
   return v;
 }
+RGSV_DI int ld_dsmem_i32(const int* local, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(ra));
+  return v;
+}
 RGSV_DI void cp_async16(void* dst, const void* src, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
                "r"(bytes)
@@ -145,6 +152,7 @@ struct ChainArgs {
   double* stats;        // per matrix: {||G||_F^2, ||B||_F^2}
   int* status;          // per matrix status bits
   int yrows;            // shared-memory rows of the Y slice (multiple of 32)
+  int* next;            // work counter (zeroed before the launch), or nullptr: static round-robin
 };
 
 // G tiles: kTR x NP, unpadded, 16-byte chunk q of row r stored at
@@ -1034,7 +1042,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_batch_chain(ChainArgs A) {
   C.init(smc, A.yrows);
   constexpr int LD = KP + 1;
   const int n = A.n, k = A.k;
-  for (int mat = cluster_idx(); mat < A.nmat; mat += cluster_count()) {
+  // Matrices are handed out by a global counter (rank 0 of the cluster draws,
+  // the peers read its draw over DSMEM): clusters that start late -- the
+  // chunked launches of rgsv_batch_gsvd share the GPU with filler kernels --
+  // simply take fewer. Which cluster computes a matrix does not change its
+  // result (every reduction inside a chain is fixed-order).
+  __shared__ int next_mat;
+  for (int it = 0;; ++it) {
+    int mat;
+    if (A.next) {
+      if (C.crank == 0 && C.tid == 0) next_mat = atomicAdd(A.next, 1);
+      __syncthreads();
+      cluster_barrier();
+      mat = ld_dsmem_i32(&next_mat, 0);  // rewritten only after the next matrix's barriers
+    } else {
+      mat = (int)cluster_idx() + it * (int)cluster_count();
+    }
+    if (mat >= A.nmat) break;
     const BatchMat g = A.mats[mat];
     const int rows = g.rows;
     const int rpc = (rows + CS - 1) / CS;
@@ -1222,11 +1246,12 @@ int batch_chain_plan(int max_rows, int n, int k, int* cs_out, int* yrows_out) {
 
 int batch_chain(const BatchMat* mats, int nmat, int max_rows, int n, int k, int q,
                 const double* omega, int64_t ldo, int64_t om_stride, double* b_out, int64_t ldb,
-                int64_t b_stride, double* stats, int* status, cudaStream_t st) {
+                int64_t b_stride, double* stats, int* status, int* next, cudaStream_t st) {
   int cs, yrows;
   if (int e = batch_chain_plan(max_rows, n, k, &cs, &yrows)) return e;
+  if (next && cudaMemsetAsync(next, 0, sizeof(int), st) != cudaSuccess) return RGSV_ERR_CUDA;
   ChainArgs a{mats, nmat, n, k, q, omega, ldo, om_stride, b_out, ldb, b_stride, stats, status,
-              yrows};
+              yrows, next};
   const int kp = k <= 16 ? 16 : 32;
   if (n <= 64) return kp == 16 ? launch_chain_np<64, 16>(a, cs, st) : launch_chain_np<64, 32>(a, cs, st);
   return kp == 16 ? launch_chain_np<128, 16>(a, cs, st) : launch_chain_np<128, 32>(a, cs, st);

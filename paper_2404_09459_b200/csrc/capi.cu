@@ -283,7 +283,7 @@ BatchLayout batch_layout(int npairs, int64_t n, int k) {
   L.omega_ws_bytes = rgsv::omega_workspace_bytes(nm, n * (int64_t)k);
   L.omega_ws = take(L.omega_ws_bytes);
   L.b = take((size_t)nm * L.kp * L.ldo * 8);
-  L.mstat = take((size_t)nm * 4);
+  L.mstat = take((size_t)(nm + 16) * 4);  // + the chain launches' work counters
   L.total = off;
   return L;
 }
@@ -316,17 +316,98 @@ int rgsv_batch_gsvd(const void* mats, int npairs, int max_rows, int64_t n, int k
   const int nm = 2 * npairs;
   if (cudaMemsetAsync(om, 0, (size_t)nm * L.kp * L.ldo * 8, st) != cudaSuccess) return RGSV_ERR_CUDA;
   if (cudaMemsetAsync(status, 0, (size_t)npairs * 4, st) != cudaSuccess) return RGSV_ERR_CUDA;
-  // Omega_i for every matrix from its own stream (pair j: seeds 2j, 2j+1)
-  if (int e = rgsv::omega_generate(seeds, nm, n, k, om, L.ldo, L.kp * L.ldo, status,
-                                   ws + L.omega_ws, L.omega_ws_bytes, st))
-    return e;
-  if (int e = rgsv::batch_chain(static_cast<const rgsv::BatchMat*>(mats), nm, max_rows, (int)n, k,
-                                q, om, L.ldo, L.kp * L.ldo, b, L.ldo, L.kp * L.ldo, stats, mstat,
-                                st))
-    return e;
   const int64_t res_stride = 6 * n + 4 + 2 * k;
-  return rgsv::launch_batch_small(b, L.ldo, L.kp * L.ldo, npairs, k, k, (int)n, classify_tol, res,
-                                  res_stride, ints, status, mstat, st);
+  const int64_t mstride = L.kp * L.ldo;
+  // pairs [c0, c0 + np): Omega_i for every matrix from its own stream (pair
+  // j: seeds 2j, 2j + 1), the clustered chain, the per-pair small GSVD
+  auto omega = [&](int c0, int np, cudaStream_t s) {
+    return rgsv::omega_generate(seeds + 2 * c0, 2 * np, n, k, om + 2 * c0 * mstride, L.ldo, mstride,
+                                status + c0, ws + L.omega_ws, L.omega_ws_bytes, s);
+  };
+  int chunk_no = 0;
+  auto chain = [&](int c0, int np, cudaStream_t s) {
+    int* next = mstat + nm + (chunk_no++ & 15);  // one work counter per chain launch
+    return rgsv::batch_chain(static_cast<const rgsv::BatchMat*>(mats) + 2 * c0, 2 * np, max_rows,
+                             (int)n, k, q, om + 2 * c0 * mstride, L.ldo, mstride,
+                             b + 2 * c0 * mstride, L.ldo, mstride, stats + 4 * c0, mstat + 2 * c0,
+                             next, s);
+  };
+  auto small = [&](int c0, int np, cudaStream_t s) {
+    return rgsv::launch_batch_small(b + 2 * c0 * mstride, L.ldo, mstride, np, k, k, (int)n,
+                                    classify_tol, res + c0 * res_stride, res_stride, ints + 4 * c0,
+                                    status + c0, mstat + 2 * c0, s);
+  };
+  // Large batches run in chunks on three streams: the chain's persistent
+  // clusters leave a dozen SMs idle (clusters must sit inside a GPC: 45 x 3
+  // of 148 SMs at cfg3), so the Omega generation of chunk c + 1 and the small
+  // GSVDs of chunk c - 1 run there while the chain of chunk c runs. The
+  // results are those of the single-launch order (the kernels are the same,
+  // per pair). Not taken under stream capture (the side streams are per call).
+  // Chunks of >= 512 pairs (>= ~22 rounds of the 45 resident clusters each,
+  // so the extra chain tails stay around 1 %).
+  constexpr int kChunks = 4;
+  const int chunks = npairs / 512 < kChunks ? npairs / 512 : kChunks;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  static const bool no_overlap = getenv("RGSV_BATCH_NO_OVERLAP") != nullptr;
+  if (chunks < 2 || no_overlap ||
+      cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    if (int e = omega(0, npairs, st)) return e;
+    if (int e = chain(0, npairs, st)) return e;
+    return small(0, npairs, st);
+  }
+  cudaStream_t s_om = nullptr, s_sm = nullptr, s_ch = nullptr;
+  int pr_least = 0, pr_greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&pr_least, &pr_greatest);
+  cudaEvent_t ev_fork = nullptr, ev_om[kChunks] = {}, ev_ch[kChunks] = {}, ev_join = nullptr;
+  int rc = 0;
+  auto ok = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == 0) rc = RGSV_ERR_CUDA;
+    return e == cudaSuccess;
+  };
+  auto mkev = [&](cudaEvent_t* e) { return ok(cudaEventCreateWithFlags(e, cudaEventDisableTiming)); };
+  // the chain runs at the highest stream priority: its clusters take the SMs
+  // the filler kernels' short blocks free, not the other way round
+  bool up = ok(cudaStreamCreateWithPriority(&s_om, cudaStreamNonBlocking, pr_least)) &&
+            ok(cudaStreamCreateWithPriority(&s_sm, cudaStreamNonBlocking, pr_least)) &&
+            ok(cudaStreamCreateWithPriority(&s_ch, cudaStreamNonBlocking, pr_greatest)) &&
+            mkev(&ev_fork) && mkev(&ev_join);
+  for (int c = 0; up && c < kChunks; ++c) up = mkev(&ev_om[c]) && mkev(&ev_ch[c]);
+  if (up) {
+    const int per = (npairs + chunks - 1) / chunks;
+    ok(cudaEventRecord(ev_fork, st));  // Omega buffer and status cleared
+    ok(cudaStreamWaitEvent(s_om, ev_fork, 0));
+    ok(cudaStreamWaitEvent(s_sm, ev_fork, 0));
+    ok(cudaStreamWaitEvent(s_ch, ev_fork, 0));
+    for (int c = 0; c < chunks && rc == 0; ++c) {
+      const int c0 = c * per, np = npairs - c0 < per ? npairs - c0 : per;
+      if (np <= 0) break;
+      if (int e = omega(c0, np, s_om)) rc = e;  // one stream: the workspace is reused in order
+      ok(cudaEventRecord(ev_om[c], s_om));
+    }
+    for (int c = 0; c < chunks && rc == 0; ++c) {
+      const int c0 = c * per, np = npairs - c0 < per ? npairs - c0 : per;
+      if (np <= 0) break;
+      ok(cudaStreamWaitEvent(s_ch, ev_om[c], 0));
+      if (int e = chain(c0, np, s_ch)) rc = e;
+      ok(cudaEventRecord(ev_ch[c], s_ch));
+      ok(cudaStreamWaitEvent(s_sm, ev_ch[c], 0));
+      if (rc == 0)
+        if (int e = small(c0, np, s_sm)) rc = e;
+    }
+    ok(cudaEventRecord(ev_join, s_sm));
+    ok(cudaStreamWaitEvent(st, ev_join, 0));  // s_om's work is ordered before the chains
+  }
+  // destroying streams / events with work in flight only defers their release
+  for (int c = 0; c < kChunks; ++c) {
+    if (ev_om[c]) cudaEventDestroy(ev_om[c]);
+    if (ev_ch[c]) cudaEventDestroy(ev_ch[c]);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (s_ch) cudaStreamDestroy(s_ch);
+  if (s_om) cudaStreamDestroy(s_om);
+  if (s_sm) cudaStreamDestroy(s_sm);
+  return rc;
 }
 
 size_t rgsv_sketch_workspace_bytes(int64_t m, int64_t n, int k) {

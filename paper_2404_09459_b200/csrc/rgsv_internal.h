@@ -53,7 +53,7 @@ struct BatchMat {
 int batch_chain_plan(int max_rows, int n, int k, int* cs_out, int* yrows_out);
 int batch_chain(const BatchMat* mats, int nmat, int max_rows, int n, int k, int q,
                 const double* omega, int64_t ldo, int64_t om_stride, double* b_out, int64_t ldb,
-                int64_t b_stride, double* stats, int* status, cudaStream_t st);
+                int64_t b_stride, double* stats, int* status, int* next, cudaStream_t st);
 
 int launch_batch_small(const double* b, int64_t ldb, int64_t b_stride, int npairs, int k1, int k2,
                        int n, double tol, double* res, int64_t res_stride, int* ints,
