@@ -345,8 +345,13 @@ int rgsv_batch_gsvd(const void* mats, int npairs, int max_rows, int64_t n, int k
   // per pair). Not taken under stream capture (the side streams are per call).
   // Chunks of >= 512 pairs (>= ~22 rounds of the 45 resident clusters each,
   // so the extra chain tails stay around 1 %).
-  constexpr int kChunks = 4;
-  const int chunks = npairs / 512 < kChunks ? npairs / 512 : kChunks;
+  constexpr int kChunks = 8;
+  static const int want_chunks = [] {
+    const char* e = getenv("RGSV_BATCH_CHUNKS");  // tuning: 2 .. 8 (default 4)
+    const int v = e ? atoi(e) : 4;
+    return v >= 2 && v <= kChunks ? v : 4;
+  }();
+  const int chunks = npairs / 512 < want_chunks ? npairs / 512 : want_chunks;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   static const bool no_overlap = getenv("RGSV_BATCH_NO_OVERLAP") != nullptr;
   if (chunks < 2 || no_overlap ||
