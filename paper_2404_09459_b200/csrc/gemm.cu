@@ -25,6 +25,21 @@
 
 namespace rgsv {
 
+// Operand fragments are read with explicit ld.shared: the staging pointers
+// come out of integer alignment arithmetic on the dynamic shared-memory base,
+// which hides their address space from the compiler -- it emitted generic
+// LD.E.64 (checked in SASS), with the generic path's address-space test and
+// the long-latency scoreboard class, instead of LDS.64.
+#ifndef RGSV_GEMM_GENERIC_LD
+RGSV_DI double lds_f64(const uint8_t* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+  return v;
+}
+#else
+RGSV_DI double lds_f64(const uint8_t* p) { return *reinterpret_cast<const double*>(p); }
+#endif
+
 constexpr int kMaxTileMap = 64;
 
 struct Decomp {
@@ -125,12 +140,12 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
       double a[MT], b[NT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        a[mt] = *reinterpret_cast<const double*>(sg + swz128_f64((wm * MT + mt) * 8 + g, kap));
+        a[mt] = lds_f64(sg + swz128_f64((wm * MT + mt) * 8 + g, kap));
         if (SUMSQ && do_ss) ss = fma(a[mt], a[mt], ss);
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
-        b[nt] = *reinterpret_cast<const double*>(sx + swz128_f64((wn * NT + nt) * 8 + g, kap));
+        b[nt] = lds_f64(sx + swz128_f64((wn * NT + nt) * 8 + g, kap));
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -262,12 +277,12 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int c = (wm * MT + mt) * 8 + g;
-        a[mt] = *reinterpret_cast<const double*>(sq + (c >> 4) * 2048 + swz128_f64(rho, c & 15));
+        a[mt] = lds_f64(sq + (c >> 4) * 2048 + swz128_f64(rho, c & 15));
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int c = (wn * NT + nt) * 8 + g;
-        b[nt] = *reinterpret_cast<const double*>(sg + (c >> 4) * 2048 + swz128_f64(rho, c & 15));
+        b[nt] = lds_f64(sg + (c >> 4) * 2048 + swz128_f64(rho, c & 15));
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
