@@ -382,6 +382,16 @@ bool exact_width_enabled() {
   return on;
 }
 
+// RGSV_TILE96=0 turns the 96-wide tiles (widths that are multiples of 96,
+// cfg4's kp = 288) off (A/B runs).
+bool tile96_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RGSV_TILE96");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 template <typename K>
 int set_smem(K kernel, size_t bytes) {
   static thread_local const void* done[64];
@@ -581,6 +591,9 @@ int gemm_gx(const GemmArgs& a0, cudaStream_t st) {
   if (a.N <= 16) return run_gx<2, 2, 8, 1, 6, false>(a, st);
   if (a.N <= 32) return run_gx<2, 4, 8, 1, 6, false>(a, st);
   if (a.N <= 64) return run_gx<4, 4, 4, 2, 6, false>(a, st);
+  // widths that are whole 96-column tiles (cfg4's kp = 288 = 3 x 96; 128-wide
+  // tiles would issue 384 columns): 12 DMMA warps of 32 x 32
+  if (tile96_enabled() && a.N > 128 && a.N % 96 == 0) return run_gx<4, 4, 4, 3, 5, false>(a, st);
   return run_gx<4, 8, 4, 2, 5, false>(a, st);
 }
 
@@ -602,6 +615,11 @@ int gemm_gtq(const GemmArgs& a0, cudaStream_t st) {
     return run_gtq<5, 2, 3, 4, 6>(a, st);
   }
   const GemmArgs& a = a0;
+  // Lower-triangular Gram whose width is whole 96-tiles (cfg4's kp = 288):
+  // 96 x 96 tiles, 12 DMMA warps of 24 x 32. The 6 tiles on or below the
+  // diagonal are 55296 entries against 90112 for the 11 live 128 x 64 tiles.
+  if (tile96_enabled() && a.lower_only && a.M == a.N && a.M >= 192 && a.M % 96 == 0)
+    return run_gtq<3, 4, 4, 3, 6>(a, st);
   if (a.N <= 16 && a.M <= 16) return run_gtq<1, 1, 2, 2, 6>(a, st);
   if (a.N <= 32 && a.M <= 32) return run_gtq<2, 2, 2, 2, 6>(a, st);
   if (a.N <= 64 && a.M <= 64) return run_gtq<4, 4, 2, 2, 6>(a, st);

@@ -228,7 +228,8 @@ def test_core_svd_and_pseudoinverse_norm(rows, cols):
             rg.pseudoinverse_norm(b)
 
 
-@pytest.mark.parametrize("rows,kp", [(100000, 288), (5000, 208), (300, 144), (2000, 64)])
+@pytest.mark.parametrize("rows,kp", [(100000, 288), (5000, 208), (300, 144), (2000, 64),
+                                     (20000, 192), (3001, 480)])
 def test_gram_lower(rows, kp):
     """rgsv_gemm_gram_lower: the lower triangle of A^T A (the CholeskyQR
     Gram the blocked Cholesky reads) to fp64 accuracy; tiles strictly above

@@ -32,6 +32,7 @@ gram = torch.zeros((kp, kp), dtype=torch.float64, device="cuda")
 q = torch.zeros((m, kp), dtype=torch.float64, device="cuda")
 linv = torch.eye(kp, dtype=torch.float64, device="cuda")
 t("gram Y^T Y (gemm_gtq, fp64)", lambda: ops.gtq(dv.vp(y), kp, dv.vp(y), kp, dv.vp(gram), kp, kp, kp, m))
+t("gram lower (rgsv_gemm_gram_lower, fp64)", lambda: ops.gram(dv.vp(y), kp, kp, m, dv.vp(gram)))
 t("trsm Y Linv (gemm_gx, fp64)", lambda: ops.gx(dv.vp(y), kp, dv.vp(linv), kp, dv.vp(q), kp, m, kp, kp))
 g = y.T @ y
 t("chol_inv (kp=%d)" % kp, lambda: ops.chol(g, k, kp, m))
