@@ -36,7 +36,8 @@ def relerr(x, y):
 
 
 GX_SHAPES = [(2000, 32, 200), (20000, 64, 1000), (129, 16, 77), (5, 64, 40), (300, 128, 64),
-             (1000, 256, 100), (64, 64, 1000), (4000, 16, 64), (16000, 64, 1000)]
+             (1000, 256, 100), (64, 64, 1000), (4000, 16, 64), (16000, 64, 1000),
+             (5003, 288, 288), (777, 192, 50), (130, 384, 96)]  # 96-wide tiles (N % 96 == 0)
 
 
 @pytest.mark.parametrize("M,N,K", GX_SHAPES)
