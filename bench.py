@@ -163,9 +163,11 @@ def cpu_baseline(cfg, budget_s: float, g1, g2):
 
 
 def workload_desc(cfg):
+    """The workload string both arms print (config.workload)."""
+    seeds = "per-pair Omega seeds 2j, 2j+1" if cfg.batch > 1 else "Omega seed = step index"
     return (f"{cfg.name}: {cfg.dtype} rGSVD pair m={cfg.m} p={cfg.p} n={cfg.n} s={cfg.s} "
             f"(shared {cfg.shared}) decay 10^(-{cfg.decay:g} j/s) eps={cfg.eps:g} k={cfg.k} "
-            f"q={cfg.q}, fixed-rank range finder, Omega seed = step index")
+            f"q={cfg.q}, fixed-rank range finder, {seeds}")
 
 
 def _all_blas_threads() -> int:
@@ -216,7 +218,8 @@ def run_reference(args, rank, world):
         "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg), "parallelism": "host cores"},
+        "config": {"workload": workload_desc(cfg), "g_bytes": cfg.g_bytes,
+                   "parallelism": "host cores"},
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{args.steps} whole pairs through the numpy restatement of "
@@ -383,8 +386,7 @@ def run_ours_batch(args, rank, world):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-generated with the workloads.py recipe)",
-            "config": {"workload": workload_desc(cfg).replace("Omega seed = step index",
-                                                              "per-pair Omega seeds 2j, 2j+1"),
+            "config": {"workload": workload_desc(cfg),
                        "batch": B, "g_bytes_total": cfg.g_bytes * B,
                        "l2": "inputs larger than L2 (%.1f GB > 126 MB)" % (cfg.g_bytes * B / 1e9),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
