@@ -6,6 +6,8 @@ device path.
     python -m paper_2404_09459_b200 compare --g1 A.mtx --g2 B.mtx [options]
     python -m paper_2404_09459_b200 extract --input A.mtx [options]
     python -m paper_2404_09459_b200 bounds  --g1 A.mtx --g2 B.mtx [--k K --oversample P]
+    python -m paper_2404_09459_b200 synth   --m M --p P --n N --field real --out-dir DIR
+    python -m paper_2404_09459_b200 bench   (--g1 A --g2 B | --m M --p P --n N --field real)
 
 Routing (cli.py:88-176): ``gsv`` -> ``compute_gsv``, ``compare`` ->
 ``compare``, ``extract`` -> ``extract_basis``, ``bounds`` -> the direct
@@ -15,10 +17,11 @@ certificates of ``bounds.py``. ``--seed`` defaults to ``RGSV_SEED`` and then
 0 (cli.py:39-44). One flag is added: ``--power-iters`` (the q of
 ``ExtractionConfig``; 0, the reference's behaviour, by default).
 
-The reference's ``synth`` and ``bench`` subcommands front its §4.1 generator
-and its timing harness, both outside this repository's scope:
-they are accepted by the parser and answer with a ``validation`` error, so a
-script that calls them fails loudly rather than silently.
+``synth`` (cli.py:113-132) writes g1.mtx, g2.mtx and the true spectrum of a
+``synthetic.synth_gmp`` pair; ``bench`` (cli.py:135-155) runs the timing
+harness of this package's ``bench`` module and prints the per-method medians.
+Both keep the reference's ``--field`` default ("complex"), which the device
+path rejects with a ``validation`` error: pass ``--field real``.
 """
 
 from __future__ import annotations
@@ -114,11 +117,43 @@ def _run_bounds(args) -> int:
     return 0
 
 
-def _run_unavailable(args) -> int:
-    raise ValidationError(
-        f"subcommand {args.command!r} fronts the reference's synthetic generator / timing "
-        "harness, which this device drop-in does not provide (use the reference package for "
-        "it, or bench.py at the repository root for timings)")
+def _run_synth(args) -> int:
+    from pathlib import Path
+
+    from .synthetic import SynthSpec, synth_gmp
+
+    spec = SynthSpec(m=args.m, p=args.p, n=args.n, rank_frac=args.rank_frac,
+                     seed=_seed_of(args), field=args.field)
+    result = synth_gmp(spec)
+    out = Path(args.out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    io.write_matrix(out / "g1.mtx", result.pair.g1.t.cpu().numpy())
+    io.write_matrix(out / "g2.mtx", result.pair.g2.t.cpu().numpy())
+    ext = "json" if args.format == "json" else "csv"
+    io.write_report(result.true_spectrum, out / f"truth.{ext}", args.format)
+    print(f"wrote {out}/g1.mtx {out}/g2.mtx {out}/truth.{ext} "
+          f"(condition_r={result.condition_r:.6g})", file=sys.stderr)
+    return 0
+
+
+def _run_bench(args) -> int:
+    from .bench import RunConfig, median_seconds, run_bench
+    from .synthetic import SynthSpec
+
+    synth = None
+    sizes = (args.m, args.p, args.n)
+    if any(v is not None for v in sizes):
+        if any(v is None for v in sizes):
+            raise ValidationError("--m, --p and --n must be given together")
+        synth = SynthSpec(m=args.m, p=args.p, n=args.n, rank_frac=args.rank_frac,
+                          seed=_seed_of(args), field=args.field)
+    cfg = RunConfig(g1_path=args.g1, g2_path=args.g2, synth=synth, options=_options(args),
+                    output=args.output, format=args.format, repetitions=args.reps)
+    records = run_bench(cfg)
+    io.write_report(records, cfg.output, cfg.format)
+    for method, sec in sorted(median_seconds(records).items()):
+        print(f"median {method}: {sec:.6f} s", file=sys.stderr)
+    return 0
 
 
 def build_parser() -> argparse.ArgumentParser:
@@ -173,17 +208,34 @@ def build_parser() -> argparse.ArgumentParser:
     gsv_flags(p), output_flags(p)
     p.set_defaults(func=_run_bounds)
 
-    for name in ("synth", "bench"):
-        p = sub.add_parser(name, help="reference-only (generator / timing harness)")
-        p.set_defaults(func=_run_unavailable)
+    p = sub.add_parser("synth", help="generate a synthetic pair with known spectrum")
+    p.add_argument("--m", type=int, required=True)
+    p.add_argument("--p", type=int, required=True)
+    p.add_argument("--n", type=int, required=True)
+    p.add_argument("--rank-frac", type=float, default=0.6)
+    p.add_argument("--seed", type=int, default=None)
+    p.add_argument("--field", choices=["real", "complex"], default="complex")
+    p.add_argument("--out-dir", required=True)
+    p.add_argument("--format", choices=["csv", "json"], default="csv")
+    p.set_defaults(func=_run_synth)
+
+    p = sub.add_parser("bench", help="time randomized vs direct")
+    p.add_argument("--g1", default=None)
+    p.add_argument("--g2", default=None)
+    p.add_argument("--m", type=int, default=None)
+    p.add_argument("--p", type=int, default=None)
+    p.add_argument("--n", type=int, default=None)
+    p.add_argument("--rank-frac", type=float, default=0.6)
+    p.add_argument("--field", choices=["real", "complex"], default="complex")
+    p.add_argument("--reps", type=int, default=1)
+    gsv_flags(p), output_flags(p)
+    p.set_defaults(func=_run_bench)
     return parser
 
 
 def main(argv=None) -> int:
     parser = build_parser()
-    args, extra = parser.parse_known_args(argv)
-    if extra and args.func is not _run_unavailable:
-        parser.error("unrecognized arguments: " + " ".join(extra))
+    args = parser.parse_args(argv)
     try:
         return args.func(args)
     except GsvError as exc:

@@ -12,19 +12,20 @@ by the other and reports serialize to the same text:
 * ``write_matrix`` (io.py:91-96): dense real Matrix Market at 17 significant
   digits, column-major, which ``read_matrix`` round-trips bitwise.
 * ``report_to_dict`` / ``write_report`` (io.py:120-264): JSON or CSV of a
-  ``ComparativeReport``, ``GsvSpectrum``, ``BoundCertificate`` or
-  ``BasisResult``, floats at ``.17g``.
+  ``ComparativeReport``, ``GsvSpectrum``, ``BoundCertificate``,
+  ``BasisResult`` or a list of the timing harness's ``BenchRecord``s, floats
+  at ``.17g``.
 
 Parsing and serialization are host work by nature; the parsed arrays go to
 the device path through ``GmpPair`` / ``extract_basis`` unchanged. Complex
 files are parsed faithfully and then rejected by the device path's
-``ValidationError`` (no CPU fallback). The reference's
-``bench_records`` serialization belongs to its timing harness (out of scope).
+``ValidationError`` (no CPU fallback).
 """
 
 from __future__ import annotations
 
 import csv
+import dataclasses
 import json
 import sys
 from pathlib import Path
@@ -231,8 +232,14 @@ def _plain(x):
     return x
 
 
+_BENCH_COLUMNS = ("method", "repetition", "seconds", "err_alpha", "err_beta", "residual1",
+                  "residual2", "l1", "l2", "m", "p", "n")
+
+
 def _kind(report) -> str:
     # late imports: io is a leaf the CLI pulls in before the device modules
+    if isinstance(report, (list, tuple)):  # the timing harness's records (io.py:171-178)
+        return "bench_records"
     from .analysis import ComparativeReport
     from .bounds import BoundCertificate
     from .engine import GsvSpectrum
@@ -253,6 +260,10 @@ def _basis_columns(report) -> int:
 def report_to_dict(report) -> dict:
     """JSON structure of a report object (io.py:120-180), key for key."""
     kind = _kind(report)
+    if kind == "bench_records":
+        return {"kind": kind,
+                "records": [{k: _plain(v) for k, v in dataclasses.asdict(rec).items()}
+                            for rec in report]}
     if kind == "comparative_report":
         spec = report.spectrum
         return {"kind": kind, "alphas": _plain(spec.alphas), "betas": _plain(spec.betas),
@@ -277,6 +288,12 @@ def report_to_dict(report) -> dict:
 def _csv_rows(report) -> list:
     """Per-index rows, then the scalar block (io.py:183-247)."""
     kind = _kind(report)
+    if kind == "bench_records":  # one row per record (io.py:236-245)
+        rows = [list(_BENCH_COLUMNS)]
+        for rec in report:
+            d = dataclasses.asdict(rec)
+            rows.append([d[k] if isinstance(d[k], str) else _num(d[k]) for k in _BENCH_COLUMNS])
+        return rows
     if kind == "comparative_report":
         spec = report.spectrum
         cols = (spec.alphas, spec.betas, report.rho, report.theta, report.p1, report.p2)

@@ -123,7 +123,9 @@ def test_error_exits(tmp_path, capsys):
     cplx = tmp_path / "c.csv"
     cplx.write_text("1+2j,0\n0,1\n")
     assert cli.main(["gsv", "--g1", str(cplx), "--g2", str(ok)]) == 5  # no complex device path
-    assert cli.main(["synth", "--m", "20"]) == 5
+    # synth with the reference's default field (complex): validation error
+    assert cli.main(["synth", "--m", "20", "--p", "20", "--n", "8", "--out-dir",
+                     str(tmp_path / "s")]) == 5
     with pytest.raises(SystemExit) as exc:
         cli.main(["gsv"])
     assert exc.value.code == 2  # argparse usage failure

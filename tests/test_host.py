@@ -282,3 +282,54 @@ def test_projector_bound_host_formula_matches_reference_golden():
             got = projector_bound(pair, spec, k=int(k), oversample=int(os_),
                                   which="first" if side == 0 else "second")
             assert got == want or abs(got - want) <= 1e-14 * abs(want)
+
+
+def test_synth_spec_and_run_config_validation():
+    """SynthSpec / RunConfig argument checks and messages of the reference
+    (synthetic.py:36-49, bench.py:31-42); no device needed."""
+    import paper_2404_09459_b200 as rg
+
+    spec = rg.SynthSpec(m=10, p=8, n=6)
+    assert spec.rank == 3 and spec.field == "complex" and spec.rank_frac == 0.6
+    for kw, msg in ((dict(m=0, p=1, n=2), "m and p must be >= 1"), (dict(m=1, p=1, n=1), "n must be"),
+                    (dict(m=2, p=2, n=2, rank_frac=0.0), "rank_frac"),
+                    (dict(m=2, p=2, n=2, rank_frac=1.5), "rank_frac"),
+                    (dict(m=2, p=2, n=2, field="quaternion"), "field must be")):
+        with pytest.raises(rg.ValidationError, match=msg):
+            rg.SynthSpec(**kw)
+    with pytest.raises(rg.InfeasibleRankError):
+        rg.synth_gmp(rg.SynthSpec(m=10, p=8, n=6, rank_frac=0.3, field="real"))
+    with pytest.raises(rg.ValidationError, match="yields empty"):
+        rg.synth_gmp(rg.SynthSpec(m=1, p=1, n=4, rank_frac=0.5, field="real"))
+    with pytest.raises(rg.ValidationError, match="complex"):
+        rg.synth_gmp(spec)
+
+    with pytest.raises(rg.ValidationError, match="given together"):
+        rg.RunConfig(g1_path="a.mtx")
+    with pytest.raises(rg.ValidationError, match="exactly one input source"):
+        rg.RunConfig()
+    with pytest.raises(rg.ValidationError, match="exactly one input source"):
+        rg.RunConfig(g1_path="a", g2_path="b", synth=spec)
+    with pytest.raises(rg.ValidationError, match="repetitions"):
+        rg.RunConfig(synth=spec, repetitions=0)
+    with pytest.raises(rg.ValidationError, match="format"):
+        rg.RunConfig(synth=spec, format="xml")
+    cfg = rg.RunConfig(synth=spec)
+    assert cfg.options == rg.GsvOptions() and cfg.repetitions == 1 and cfg.format == "csv"
+
+    recs = [rg.BenchRecord("direct", i, s, 0.0, 0.0, None, None, 4, 4, 4, 4, 2)
+            for i, s in enumerate((3.0, 1.0, 2.0))]
+    recs.append(rg.BenchRecord("randomized", 0, 5.0, 0.0, 0.0, 1e-9, 1e-9, 2, 2, 4, 4, 2))
+    assert rg.median_seconds(recs) == {"direct": 2.0, "randomized": 5.0}
+
+
+def test_true_spectrum_layout():
+    """alpha = (ones, interior, zeros), beta exact 0 / 1 in the outer blocks
+    (synthetic.py:85-89)."""
+    from paper_2404_09459_b200.synthetic import true_spectrum
+
+    sp = true_spectrum(6, 4, np.array([0.8, 0.3]))
+    assert (sp.r, sp.s, sp.n) == (2, 2, 6)
+    assert list(sp.alphas) == [1.0, 1.0, 0.8, 0.3, 0.0, 0.0]
+    assert list(sp.betas[:2]) == [0.0, 0.0] and list(sp.betas[4:]) == [1.0, 1.0]
+    assert np.allclose(sp.alphas**2 + sp.betas**2, 1.0, atol=1e-15)
