@@ -7,7 +7,8 @@ right factor, then the two left blocks: synthetic.py:84-99), so a seed names
 the same pair here and there; the linear algebra runs on the B200 through
 this package's own kernels -- ``core.reduced_qr`` for the orthonormal left
 blocks (synthetic.py:102-103), the DMMA ``rgsv_gemm_gx`` for the two products
-(synthetic.py:106-107) and the device Jacobi for cond(R*) (synthetic.py:109).
+(synthetic.py:106-107) and the device Jacobi (values only) for cond(R*)
+(synthetic.py:109).
 The pair matches the reference's to rounding (the QR kernels are not LAPACK's);
 the true spectrum is bit-identical.
 
@@ -128,7 +129,11 @@ def synth_gmp(spec: SynthSpec) -> SynthResult:
     g1 = _scaled_product(u_active, spectrum.alphas[:rank], r_star[:rank])
     g2 = _scaled_product(v_active, spectrum.betas[n - rank:], r_star[n - rank:])
 
-    sr = core.svd(r_star).s
+    # cond(R*) from the singular values alone (device Jacobi, no vectors)
+    from .validation import _jacobi_values
+
+    rd = _dev.to_device(r_star, "r_star")
+    sr = _jacobi_values(rd.t.clone(), n, n)
     return SynthResult(GmpPair(g1, g2), spectrum, float(sr[0] / sr[-1]))
 
 

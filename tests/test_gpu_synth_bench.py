@@ -108,3 +108,16 @@ def test_cli_synth_then_bench(tmp_path, capsys):
     # the reference's default field is complex: rejected loudly (exit code 5)
     assert cli.main(["synth", "--m", "30", "--p", "24", "--n", "10", "--out-dir", str(out)]) == 5
     assert cli.main(["bench", "--m", "30", "--p", "24"]) == 5
+
+
+def test_synth_large_pair_spectrum_recovered():
+    """A size beyond the Householder route (rows > 1408: CholeskyQR3 left
+    blocks, 128-wide GEMM tiles): orthogonality of the construction shows in
+    the direct method recovering the prescribed spectrum."""
+    res = rg.synth_gmp(rg.SynthSpec(m=3000, p=2500, n=600, rank_frac=0.7, seed=9, field="real"))
+    assert res.pair.m == 3000 and res.pair.p == 2500 and res.pair.n == 600
+    spec = rg.compute_gsv(res.pair, rg.GsvOptions(method="direct"))
+    assert (spec.r, spec.s) == (res.true_spectrum.r, res.true_spectrum.s) == (180, 240)
+    tol = 1e-13 * res.condition_r * 10
+    assert np.max(np.abs(spec.alphas - res.true_spectrum.alphas)) <= tol
+    assert np.max(np.abs(spec.betas - res.true_spectrum.betas)) <= tol
