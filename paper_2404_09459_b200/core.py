@@ -161,7 +161,7 @@ def tall_qr(a: torch.Tensor, rows: int, cols: int):
     y = torch.zeros((rows, kp), dtype=torch.float64, device="cuda")
     y[:, :cols].copy_(a[:, :cols])
     try:
-        _qr_in_place(y, rows, cols)
+        _qr_in_place(y, rows, cols, orig=a)
         q = y[:, :cols]
         r = torch.triu(_gemm_at_b(q, a, cols, cols, rows))
         d = torch.diagonal(r).abs()
@@ -189,9 +189,18 @@ def tall_qr(a: torch.Tensor, rows: int, cols: int):
     return q, torch.triu(r)
 
 
-def _qr_in_place(y: torch.Tensor, rows: int, k: int) -> None:
+def _qr_in_place(y: torch.Tensor, rows: int, k: int, orig: torch.Tensor | None = None) -> None:
     """Shifted CholeskyQR3 on the device through the C-ABI building blocks;
-    y (rows x kp) is replaced by Q. RankDeficiencyError on breakdown."""
+    y (rows x kp) is replaced by Q. RankDeficiencyError on breakdown.
+
+    Shifted CholeskyQR3 needs cond(Q1)^2 * n * u < 1 for its unshifted second
+    pass, which fails from cond(Y) ~ 1e10 at n ~ 1000 although Y has full
+    numerical rank (the reference accepts stacks up to 1e12, engine.py:57).
+    With ``orig`` (the untouched input) a breakdown is retried with a second
+    shifted pass, shift / shift / plain / plain: each shifted pass takes the
+    condition number down by ~sqrt(shift), so the plain passes see
+    cond <~ 1e5 for any input up to ~1/u. A genuinely rank-deficient matrix
+    still breaks down in the plain passes and raises."""
     L = lib()
     kp = y.shape[1]
     st = _dev.sp(torch.cuda.current_stream())
@@ -200,19 +209,32 @@ def _qr_in_place(y: torch.Tensor, rows: int, k: int) -> None:
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     scratch = _scratch_for(kp)
     tmp = torch.empty_like(y)
-    src, dst = y, tmp
-    for step in range(3):
-        check(L.rgsv_gemm_gtq(_dev.vp(src), kp, _dev.vp(src), kp, _dev.vp(gram), kp, kp, kp, rows,
-                              _dev.vp(scratch), scratch.numel() * 8, st), "gram")
-        check(L.rgsv_chol_inv(_dev.vp(gram), k, kp, rows if step == 0 else 0, _dev.vp(linv),
-                              None, None, _dev.vp(status), st), "chol")
-        check(L.rgsv_gemm_gx(_dev.vp(src), kp, _dev.vp(linv), kp, _dev.vp(dst), kp, rows, kp, kp,
-                             _dev.vp(scratch), scratch.numel() * 8, st), "trsm")
-        src, dst = dst, src
-    if int(status.item()) != 0:
-        raise RankDeficiencyError("CholeskyQR breakdown: matrix is numerically rank deficient")
-    if src is not y:
-        y.copy_(src)
+
+    def passes(shifts) -> bool:
+        src, dst = y, tmp
+        for shift_rows in shifts:
+            check(L.rgsv_gemm_gtq(_dev.vp(src), kp, _dev.vp(src), kp, _dev.vp(gram), kp, kp, kp,
+                                  rows, _dev.vp(scratch), scratch.numel() * 8, st), "gram")
+            check(L.rgsv_chol_inv(_dev.vp(gram), k, kp, shift_rows, _dev.vp(linv), None, None,
+                                  _dev.vp(status), st), "chol")
+            check(L.rgsv_gemm_gx(_dev.vp(src), kp, _dev.vp(linv), kp, _dev.vp(dst), kp, rows, kp,
+                                 kp, _dev.vp(scratch), scratch.numel() * 8, st), "trsm")
+            src, dst = dst, src
+        if int(status.item()) != 0:
+            return False
+        if src is not y:
+            y.copy_(src)
+        return True
+
+    if passes((rows, 0, 0)):
+        return
+    if orig is not None:
+        y.zero_()
+        y[:, :k].copy_(orig[:, :k])
+        status.zero_()
+        if passes((rows, rows, 0, 0)):
+            return
+    raise RankDeficiencyError("CholeskyQR breakdown: matrix is numerically rank deficient")
 
 
 __all__ = ["REAL", "COMPLEX", "QrFactors", "SvdFactors", "as_matrix", "gaussian_matrix",
@@ -264,7 +286,7 @@ def pseudoinverse_norm(m) -> float:
             raise
         y = torch.zeros((rows, _dev.ceil16(cols)), dtype=torch.float64, device="cuda")
         y[:, :cols] = g.t
-        _qr_in_place(y, rows, cols)  # raises RankDeficiencyError
+        _qr_in_place(y, rows, cols, orig=g.t)  # raises RankDeficiencyError
         r = _gemm_at_b(y[:, :cols], g.t, cols, cols, rows)
         sv = _jacobi_values(torch.triu(r).contiguous(), cols, cols)
     smax, smin = float(sv[0]), float(sv[-1])

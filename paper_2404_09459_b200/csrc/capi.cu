@@ -716,8 +716,12 @@ int rgsv_small_gsvd(const double* b1, int64_t ldb1, int l1, const double* b2, in
     const int64_t kpn = L.kpn;
     if (kpn > kCholMaxKp) return RGSV_ERR_DIMENSION;  // blocked Cholesky limit
     if (int e = launch_stack(S, kpn, b1, ldb1, l1, b2, ldb2, l2, l, n, st)) return e;
+    // The direct method stacks the pair itself here: any stack the reference
+    // accepts (sigma_min > 1e-12 sigma_max, engine.py:57) must factor, so two
+    // shifted passes and two plain ones (CholeskyQR3 proper stops at
+    // cond ~ 1e10 for n ~ 1000).
     if (int e = cholqr3_tall(S, S2, l, (int)n, (int)kpn, gram, linv, rdiag, scratch, sb, status,
-                             &Q, st))
+                             &Q, st, 4, nullptr, -1, 2))
       return e;
     ldq = kpn;
     r = (int)n;

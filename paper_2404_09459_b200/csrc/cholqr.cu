@@ -1145,7 +1145,7 @@ static int tall_gram_split() {
 int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram, double* linv,
                  double* rdiag, double* scratch, size_t scratch_bytes, int* status,
                  double** q_out, cudaStream_t st, int passes, const Reducer* red,
-                 int64_t shift_rows) {
+                 int64_t shift_rows, int shifted_passes) {
   if (shift_rows < 0) shift_rows = m;
   double* src = y;
   double* dst = tmp;
@@ -1171,8 +1171,9 @@ int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram,
     if (int e = gemm_gtq(g, st)) return e;
     if (red)  // sum the Gram partials of every rank's row block
       if (int e = (*red)(gram, (int64_t)kp * kp, st)) return e;
-    if (int e = chol_inv(gram, k, kp, step == 0 ? shift_rows : 0, linv, nullptr, nullptr,
-                         step == 0 ? rdiag : nullptr, step == 0 ? nullptr : rdiag, status, st))
+    if (int e = chol_inv(gram, k, kp, step < shifted_passes ? shift_rows : 0, linv, nullptr,
+                         nullptr, step == 0 ? rdiag : nullptr, step == 0 ? nullptr : rdiag, status,
+                         st))
       return e;
     GemmArgs t;
     t.A = src;

@@ -84,7 +84,10 @@ struct Workspace {
 // whose span (and nested leading spans) is all that is used downstream.
 // Row-sharded use: `red` all-reduces each pass's Gram partial over the
 // ranks (Y is this rank's row block) and `shift_rows` is the global row
-// count of the shift (defaults to m).
+// count of the shift (defaults to m). `shifted_passes` > 1 shifts that many
+// leading passes: with passes = 4 and two shifted passes the factorisation
+// survives cond(Y) up to ~1/u (the unshifted second pass of CholeskyQR3
+// needs cond(Q1)^2 n u < 1, i.e. cond(Y) <~ 1e10 at n ~ 1000).
 struct Reducer {
   rgsv_allreduce_fn fn = nullptr;
   void* ctx = nullptr;
@@ -97,7 +100,7 @@ struct Reducer {
 int cholqr3_tall(double* y, double* tmp, int64_t m, int k, int kp, double* gram, double* linv,
                  double* rdiag, double* scratch, size_t scratch_bytes, int* status,
                  double** q_out, cudaStream_t st, int passes = 3, const Reducer* red = nullptr,
-                 int64_t shift_rows = -1);
+                 int64_t shift_rows = -1, int shifted_passes = 1);
 
 // Shifted CholeskyQR3 of Z = B^T where B is kp x n row-major (ld ldn):
 // returns Qhat^T (kp x n) in *qt_out (one of b / tmp).

@@ -72,7 +72,7 @@ def stacked_r(g1: "_dev.DevMatrix", g2: "_dev.DevMatrix"):
     y[g1.rows:, :n].copy_(a2)
     s0 = y.clone()
     try:
-        _qr_in_place(y, rows, n)
+        _qr_in_place(y, rows, n, orig=s0)
     except RankDeficiencyError:
         return None
     return torch.triu(_gemm_at_b(y[:, :n], s0, n, n, rows))

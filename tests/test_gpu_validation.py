@@ -112,3 +112,39 @@ def test_svd_with_vectors_blocked(rows, cols):
     assert np.linalg.norm((f.u * f.s) @ f.v.T - a) <= 1e-12 * np.linalg.norm(a)
     assert np.linalg.norm(f.u.T @ f.u - np.eye(k)) <= 1e-11 * np.sqrt(k)
     assert np.linalg.norm(f.v.T @ f.v - np.eye(k)) <= 1e-11 * np.sqrt(k)
+
+
+@pytest.mark.parametrize("rows,n,smin", [(3000, 300, 3e-12), (6000, 1100, 2e-11)])
+def test_ill_conditioned_full_rank_stack_is_accepted(rows, n, smin):
+    """A stack with sigma_min / sigma_max above the reference's 1e-12 rank
+    threshold (engine.py:57-61) is a valid pair, however ill conditioned: the
+    CholeskyQR3 route used beyond 1408 stacked rows breaks down there in its
+    unshifted second pass and is retried with two shifted passes (found by
+    tools/fuzz_parity.py: such pairs were rejected as rank deficient)."""
+    rng = np.random.default_rng(rows + n)
+    u, _ = np.linalg.qr(rng.standard_normal((rows, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = np.logspace(0.0, np.log10(smin), n)
+    s = (u * sig) @ v.T
+    cut = rows * 3 // 5
+    pair = rg.GmpPair(s[:cut], s[cut:])  # must not raise
+    sv = np.linalg.svd(s, compute_uv=False)
+    assert abs(pair.stack_norm2 - sv[0]) <= 1e-12 * sv[0]
+    assert abs(1.0 / pair.stack_pinv_norm - sv[-1]) <= 0.05 * sv[-1]
+    # ... and the direct method factors it (stacked QR beyond the Householder
+    # rows: two shifted + two plain CholeskyQR passes), at the conditioning-
+    # scaled distance from the oracle's LAPACK result
+    spec = rg.compute_gsv(pair, rg.GsvOptions(method="direct"))
+    o = orc.run_pipeline(s[:cut], s[cut:], direct=True)
+    tol = 200.0 * 2.220446049250313e-16 * sv[0] / sv[-1]
+    assert (spec.r, spec.s) == (o.r, o.s)
+    assert np.max(np.abs(spec.alphas - o.alphas)) <= tol
+    pl = rg.engine._run_pipeline(pair, rg.GsvOptions(method="direct"))
+    q = np.vstack([pl.l1_block, pl.l2_block])
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-12 * np.sqrt(n)
+    # the same matrix pushed below the threshold is still rejected
+    sig2 = sig.copy()
+    sig2[-1] = 1e-14
+    s2 = (u * sig2) @ v.T
+    with pytest.raises(rg.RankDeficiencyError):
+        rg.GmpPair(s2[:cut], s2[cut:])
