@@ -79,3 +79,81 @@ def test_random_pairs_vs_oracle(sweep_seed):
         assert np.max(np.abs(spec.alphas - o.alphas)) <= tol, tag
         assert np.max(np.abs(spec.betas - o.betas)) <= tol, tag
     assert floor_cases <= adaptive // 2, (floor_cases, adaptive)
+
+
+def test_random_batches_vs_oracle():
+    """compare_batch / run_device_batch on random small shapes (k = 2..32,
+    n on both sides of 2k, q = 0..2, 1..6 pairs, ragged rows): GSVs against
+    the oracle at the conditioning-scaled tolerance, ||G||_F to 1e-13 and the
+    captured energy to 1e-8 (the trailing sketch directions of a
+    low-rank-plus-noise matrix have no spectral gap, so the energy is only
+    determined to that level)."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    for idx in range(24):
+        k = int(rng.integers(2, 33))
+        if rng.random() < 0.6:
+            n = int(rng.integers(max(4, k), 2 * k + 1))
+        else:
+            n = int(rng.integers(2 * k + 1, 131))
+        q = int(rng.integers(0, 3))
+        m = int(rng.integers(max(k, n // 2), 5000))
+        p = int(rng.integers(max(k, n // 2), 5000))
+        if m + p < n:
+            m = n
+        nb = int(rng.integers(1, 7))
+        s = int(rng.integers(1, max(2, min(m, p, n) // 2 + 1)))
+        noise = float(rng.choice([1e-3, 1e-6, 1e-8]))
+        tag = f"batch case {idx}: B={nb} m={m} p={p} n={n} k={k} q={q} s={s} noise={noise:g}"
+        hosts = [make_pair(rng, m, p, n, s, noise) for _ in range(nb)]
+        seeds = [int(x) for x in rng.integers(0, 10000, nb)]
+        pairs = [rg.GmpPair.resident(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+                 for a, b in hosts]
+        opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(k, 0, q))
+        runs = rg.engine.run_device_batch(pairs, opts, seeds)
+        reps = rg.compare_batch(pairs, opts, seeds)
+        for j, (g1, g2) in enumerate(hosts):
+            o = orc.run_pipeline(g1, g2, k=k, q=q, seed=seeds[j])
+            sv = np.linalg.svd(np.vstack([g1, g2]), compute_uv=False)
+            tol = max(1e-11, 200.0 * EPS * sv[0] / sv[-1])
+            sp = reps[j].spectrum
+            assert (sp.r, sp.s) == (o.r, o.s), tag
+            assert np.max(np.abs(sp.alphas - o.alphas)) <= tol, tag
+            assert np.max(np.abs(reps[j].theta - orc.comparative(o.alphas, o.betas, o.r)[1])) \
+                <= 10 * tol, tag
+            for basis, ob in ((runs[j].basis1, o.basis1), (runs[j].basis2, o.basis2)):
+                h, ho = basis.residual_history, ob.residual_history
+                assert abs(h[0] - ho[0]) <= 1e-13 * ho[0], tag
+                e, eo = h[0] ** 2 - h[1] ** 2, ho[0] ** 2 - ho[1] ** 2
+                assert abs(e - eo) <= 1e-8 * eo, tag
+
+
+def test_random_recoveries():
+    """recover_gsvd on random Gaussian pairs and on synth_gmp pairs with zero
+    blocks (both methods): reconstruction and orthogonality at 1e-8, the
+    reference's acceptance level (test_engine.py:183-230)."""
+    rng = np.random.default_rng(12)
+    for idx in range(16):
+        n = int(rng.integers(3, 200))
+        method = str(rng.choice(["direct", "randomized"]))
+        m = int(rng.integers(n, 1300))
+        p = int(rng.integers(n, 1300))
+        if rng.random() < 0.5:
+            g1, g2 = rng.standard_normal((m, n)), rng.standard_normal((p, n))
+            pair = rg.GmpPair(g1, g2)
+        else:
+            frac = float(rng.uniform(0.55, 1.0))
+            pair = rg.synth_gmp(rg.SynthSpec(m=m, p=p, n=n, rank_frac=frac,
+                                             seed=int(rng.integers(0, 999)), field="real")).pair
+            g1, g2 = pair.g1.t.cpu().numpy(), pair.g2.t.cpu().numpy()
+        tag = f"recover case {idx}: m={m} p={p} n={n} {method}"
+        fac = rg.recover_gsvd(pair, rg.GsvOptions(
+            method=method, extraction=rg.ExtractionConfig(tol=1e-12, seed=idx)))
+        a, b = fac.spectrum.alphas, fac.spectrum.betas
+        assert np.linalg.norm(fac.u @ (a[:, None] * fac.r_factor) - g1) \
+            <= 1e-8 * np.linalg.norm(g1), tag
+        assert np.linalg.norm(fac.v @ (b[:, None] * fac.r_factor) - g2) \
+            <= 1e-8 * np.linalg.norm(g2), tag
+        assert np.linalg.norm(fac.u.T @ fac.u - np.eye(n)) <= 1e-8 * np.sqrt(n), tag
+        assert np.linalg.norm(fac.v.T @ fac.v - np.eye(n)) <= 1e-8 * np.sqrt(n), tag
