@@ -489,7 +489,14 @@ def run_device_pipeline(pair: GmpPair, opts: GsvOptions, *, sync: bool = True) -
     plan = _dev.pair_plan(pair.m, pair.p, pair.n, k1, k2)
     cfg = opts.extraction
     pk = plan.run(pair.g1, pair.g2, cfg.seed, cfg.power_iters, opts.classify_tol, sync=sync)
-    return unpack(pk, plan, opts)
+    try:
+        return unpack(pk, plan, opts)
+    except RankDeficiencyError:
+        # A sketch wider than the matrix's numerical rank (exactly low-rank
+        # input, trim_tol = 0) breaks CholeskyQR; the reference's Householder
+        # QR keeps such columns (rangefinder.py:119-124). The general path
+        # factors those blocks with the Householder kernel.
+        return _general_run(pair, opts)
 
 
 def unpack(pk, plan, opts: GsvOptions) -> DeviceRun:

@@ -409,10 +409,16 @@ def extract_basis(g, cfg: ExtractionConfig | None = None, *, device_result: bool
     if normf == 0.0 or normf < tol:  # rangefinder.py:96: no sampling at all
         q0 = torch.zeros((m, 0), dtype=torch.float64, device="cuda")
         return BasisResult(q0 if device_result else q0.cpu().numpy(), [normf], True, 0, [])
-    if code & 0x1:
-        raise RankDeficiencyError("CholeskyQR breakdown in the range finder (rank-deficient sketch)")
     if code & ST_NONFINITE:
         raise ValidationError("g contains non-finite entries")
+    if code & 0x1:
+        # the sketch is wider than the numerical rank of g (exactly low-rank
+        # input): CholeskyQR breaks down where the reference's Householder QR
+        # keeps the columns (rangefinder.py:119-124, trim_tol = 0); the general
+        # loop factors such a block with the Householder kernel
+        q, _, res = adaptive_device(a, cfg)
+        res.q = q if device_result else q.cpu().numpy()
+        return res
     hist = _dev.residual_history(gf2, energy)
     q = plan.q[:, :width]
     return BasisResult(q if device_result else q.cpu().numpy(), hist, hist[-1] < tol, 1, [width])

@@ -157,3 +157,90 @@ def test_random_recoveries():
             <= 1e-8 * np.linalg.norm(g2), tag
         assert np.linalg.norm(fac.u.T @ fac.u - np.eye(n)) <= 1e-8 * np.sqrt(n), tag
         assert np.linalg.norm(fac.v.T @ fac.v - np.eye(n)) <= 1e-8 * np.sqrt(n), tag
+
+
+def test_random_extractions_vs_oracle():
+    """extract_basis with random options (tol away from the estimator's
+    sqrt(eps) floor, blocksize 1..200, max_cols, trim_tol) on exact-low-rank,
+    decaying and Gaussian inputs: the same loop decisions (block widths,
+    iterations, convergence flag) and residual history as the oracle's
+    Alg. 1, an orthonormal basis and a residual estimate that matches the
+    explicit one. (With trim_tol = 0 an exactly low-rank input whose last
+    block reaches past the rank makes both implementations orthonormalise
+    pure rounding noise -- the oracle itself then returns a basis 2e-2 to
+    7e-2 from orthonormal, tools/extract_diag.py -- so that combination is
+    left to the loop comparison.)"""
+    rng = np.random.default_rng(21)
+    for idx in range(40):
+        m = int(rng.integers(2, 3000))
+        n = int(rng.integers(2, 400))
+        kind = str(rng.choice(["lowrank", "decay", "gauss"]))
+        if kind == "lowrank":
+            r = int(rng.integers(1, max(2, min(m, n) // 2)))
+            g = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+        elif kind == "decay":
+            r = min(m, n)
+            u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+            v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+            g = (u * 10.0 ** (-6.0 * np.arange(r) / r)) @ v.T
+        else:
+            g = rng.standard_normal((m, n))
+        blocksize = int(rng.choice([1, 3, 8, 17, 50, 100, 128, 200]))
+        max_cols = None if rng.random() < 0.5 else int(rng.integers(1, min(m, n) + 1))
+        gn = float(np.linalg.norm(g))
+        tol = None if rng.random() < 0.3 else gn * 10.0 ** rng.uniform(-6, -1)
+        trim_tol = float(rng.choice([1e-12, 1e-8, 0.0]))
+        seed = int(rng.integers(0, 1000))
+        tag = (f"extract case {idx}: {kind} {m}x{n} bs={blocksize} max_cols={max_cols} "
+               f"tol={tol} trim={trim_tol:g} seed={seed}")
+        res = rg.extract_basis(g, rg.ExtractionConfig(tol=tol, blocksize=blocksize, seed=seed,
+                                                      max_cols=max_cols, trim_tol=trim_tol))
+        ob = orc.extract_basis(g, tol, blocksize, seed, max_cols, trim_tol, 0)
+        if tol is not None:
+            assert list(res.block_widths) == list(ob.block_widths), tag
+            assert (res.converged, res.iterations) == (ob.converged, ob.iterations), tag
+            assert np.max(np.abs(np.array(res.residual_history)
+                                 - np.array(ob.residual_history))) <= 1e-6 * gn, tag
+        elif kind == "gauss":
+            # default tol = 1e-10 |G| is below the estimator's floor: a Gaussian
+            # matrix runs to the full width either way; the final flag is the
+            # reference's own coin flip (DESIGN.md section 2)
+            assert list(res.block_widths) == list(ob.block_widths), tag
+            assert res.iterations == ob.iterations, tag
+        if kind == "lowrank" and trim_tol == 0.0:
+            continue
+        q = res.q
+        k = q.shape[1]
+        if k:
+            assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-10 * np.sqrt(k), tag
+        true_res = np.linalg.norm(g - q @ (q.T @ g)) if k else gn
+        assert abs(true_res - res.residual_history[-1]) <= 2e-7 * gn, tag
+
+
+def test_random_core_factorizations():
+    """core.reduced_qr / svd / pseudoinverse_norm / frobenius_norm on random
+    tall, square and wide shapes against numpy (LAPACK with the reference's
+    phase fix)."""
+    rng = np.random.default_rng(22)
+    for idx in range(30):
+        rows = int(rng.integers(1, 2500))
+        cols = int(rng.integers(1, 300))
+        if rng.random() < 0.3:
+            rows, cols = cols, rows
+        a = rng.standard_normal((rows, cols))
+        tag = f"core case {idx}: {rows}x{cols}"
+        k = min(rows, cols)
+        qf = rg.reduced_qr(a)
+        q_ref, r_ref = orc.reduced_qr(a)
+        assert qf.q.shape == q_ref.shape and qf.r.shape == r_ref.shape, tag
+        assert np.linalg.norm(qf.q @ qf.r - a) <= 1e-12 * np.linalg.norm(a), tag
+        assert np.linalg.norm(qf.q.T @ qf.q - np.eye(k)) <= 1e-12 * np.sqrt(k), tag
+        assert np.max(np.abs(qf.r - r_ref)) <= 1e-10 * np.abs(r_ref).max(), tag
+        assert abs(rg.frobenius_norm(a) - np.linalg.norm(a)) <= 1e-14 * np.linalg.norm(a), tag
+        if k <= 400:
+            sf = rg.svd(a)
+            s_ref = np.linalg.svd(a, compute_uv=False)
+            assert np.max(np.abs(sf.s - s_ref)) <= 1e-12 * s_ref[0], tag
+            assert np.linalg.norm((sf.u * sf.s) @ sf.v.T - a) <= 1e-11 * np.linalg.norm(a), tag
+            if rows >= cols:
+                assert abs(rg.pseudoinverse_norm(a) - 1.0 / s_ref[-1]) <= 1e-9 / s_ref[-1], tag

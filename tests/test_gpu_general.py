@@ -247,3 +247,27 @@ def test_adaptive_power_iters_matches_oracle(rg):
     e_d = np.array(d.residual_history) ** 2
     e_o = np.array(o.residual_history) ** 2
     assert np.max(np.abs(e_d - e_o)) <= 1e-12 * nrm ** 2
+
+
+def test_sketch_wider_than_rank_keeps_columns_like_reference(rg):
+    """Exactly low-rank input, fixed width above the rank, trim_tol = 0: the
+    reference's Householder QR keeps all `width` columns (rangefinder.py:
+    119-124); the fused CholeskyQR path breaks down there and must fall back
+    to the general loop instead of raising (found by the randomized sweep).
+    The captured energy and the spectrum agree with the oracle."""
+    rng = np.random.default_rng(5)
+    g1 = rng.standard_normal((900, 6)) @ rng.standard_normal((6, 80))
+    g2 = rng.standard_normal((700, 6)) @ rng.standard_normal((6, 80)) \
+        + 1e-3 * rng.standard_normal((700, 80))
+    cfg = rg.ExtractionConfig.fixed_rank(20, 3, 0)
+    res = rg.extract_basis(g1, cfg)
+    ob = orc.fixed_rank_basis(g1, 20, 0, 3)
+    assert res.q.shape == ob.q.shape == (900, 20) and res.block_widths == [20]
+    assert abs(res.residual_history[0] - ob.residual_history[0]) <= 1e-13 * ob.residual_history[0]
+    # the 6 real directions span range(g1): nothing of g1 is left
+    assert np.linalg.norm(g1 - res.q @ (res.q.T @ g1)) <= 1e-7 * np.linalg.norm(g1)
+    assert np.linalg.norm(res.q[:, :6].T @ res.q[:, :6] - np.eye(6)) <= 1e-12
+    spec = rg.compute_gsv(rg.GmpPair(g1, g2, check_rank=False),
+                          rg.GsvOptions(extraction=cfg))
+    o = orc.run_pipeline(g1, g2, k=20, q=0, seed=3)
+    assert (spec.r, spec.s) == (o.r, o.s)
