@@ -42,18 +42,24 @@ def extract_case(rng, idx):
     ob = orc.extract_basis(g, tol, blocksize, seed, max_cols, trim_tol, 0)
     msgs = []
     gn = np.linalg.norm(g)
-    if tol is None and kind != "gauss":
-        # default tol = 1e-10 |G| sits below the estimator's floor: only check invariants
-        pass
-    else:
-        if list(res.block_widths) != list(ob.block_widths) or res.converged != ob.converged \
-                or res.iterations != ob.iterations:
-            msgs.append(f"loop differs: widths {res.block_widths} vs {ob.block_widths}, "
-                        f"conv {res.converged}/{ob.converged}")
-        elif len(res.residual_history) != len(ob.residual_history) or \
-                np.max(np.abs(np.array(res.residual_history) - np.array(ob.residual_history))) \
-                > 1e-6 * gn:
-            msgs.append(f"history differs {res.residual_history[-3:]} vs {ob.residual_history[-3:]}")
+    # default tol = 1e-10 |G| sits below the estimator's sqrt(eps) floor: the
+    # final converged flag is the reference's own coin flip there
+    if tol is None:
+        if kind == "gauss" and (list(res.block_widths) != list(ob.block_widths)
+                                or res.iterations != ob.iterations):
+            msgs.append(f"loop differs: widths {res.block_widths} vs {ob.block_widths}")
+    elif list(res.block_widths) != list(ob.block_widths) or res.converged != ob.converged \
+            or res.iterations != ob.iterations:
+        msgs.append(f"loop differs: widths {res.block_widths} vs {ob.block_widths}, "
+                    f"conv {res.converged}/{ob.converged}")
+    elif len(res.residual_history) != len(ob.residual_history) or \
+            np.max(np.abs(np.array(res.residual_history) - np.array(ob.residual_history))) \
+            > 1e-6 * gn:
+        msgs.append(f"history differs {res.residual_history[-3:]} vs {ob.residual_history[-3:]}")
+    if kind == "lowrank" and trim_tol == 0.0:
+        # columns kept past the rank are orthonormalised rounding noise in both
+        # implementations (tools/extract_diag.py): no invariant to check
+        return not msgs, desc + " " + "; ".join(msgs)
     q = res.q
     k = q.shape[1]
     if k and np.linalg.norm(q.T @ q - np.eye(k)) > 1e-10 * np.sqrt(k):
