@@ -807,6 +807,7 @@ struct BJacJob {
   int cluster;    // 1: the job is one thread-block cluster (hardware barrier)
   double* acc;    // optional nv x nv accumulated rotations (starts at I), ld ldacc
   int64_t ldacc;
+  unsigned long long* gmax;  // zeroed: bits of the largest squared row norm at entry
 };
 
 RGSV_DI int rr_player(int p, int round, int nplayers) {
@@ -818,8 +819,13 @@ constexpr int kBjPart = 8 * 10 * 64;
 constexpr size_t kBjSmem = (size_t)(kBjPart + 2 * 32 * 33) * 8;
 
 // Process the block pair (ba, bb): returns 1 if it rotated.
+// floor2: rows whose squared norm is at or below it count as zero rows (they
+// are neither rotated nor held against convergence). A rank-deficient input
+// leaves rows of pure rounding noise (~eps |A|), re-injected by every block
+// rotation they share with a large row, which can never become orthogonal
+// relative to their own size.
 __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm, int* s_flag,
-                       int inner_sweeps) {
+                       int inner_sweeps, double floor2) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* part = sm;
   double* Gm = sm + kBjPart;
@@ -876,7 +882,8 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
     const int i = e >> 5, j = e & 31;
     if (i < j) {
       const double d = Gm[i * 33 + j];
-      if (d != 0.0 && fabs(d) > tol * sqrt(Gm[i * 33 + i] * Gm[j * 33 + j])) *s_flag = 1;
+      const double gi = Gm[i * 33 + i], gj = Gm[j * 33 + j];
+      if (d != 0.0 && fmin(gi, gj) > floor2 && fabs(d) > tol * sqrt(gi * gj)) *s_flag = 1;
     }
     R[i * 33 + j] = (i == j) ? 1.0 : 0.0;
   }
@@ -892,7 +899,7 @@ __device__ int bj_pair(const BJacJob& J, int ba, int bb, double tol, double* sm,
       const int a = rr_player(pr, round, 32), b = rr_player(31 - pr, round, 32);
       const double al = Gm[a * 33 + a], be = Gm[b * 33 + b], ga = Gm[a * 33 + b];
       // |ga| > tol sqrt(al be), squared (al, be >= 0): no sqrt on the chain
-      const bool rot = ga != 0.0 && ga * ga > (tol * tol) * (al * be);
+      const bool rot = ga != 0.0 && fmin(al, be) > floor2 && ga * ga > (tol * tol) * (al * be);
       double c = 1.0, s = 0.0, tt = 0.0;
       if (rot) {
         const double zeta = (be - al) / (2.0 * ga);
@@ -1023,6 +1030,29 @@ __global__ void __launch_bounds__(kDenseThreads) k_bjacobi(BJacJob j0, BJacJob j
   const int nbe = nblk + (nblk & 1);
   const int npairs = nbe / 2;
   unsigned epoch = 0;
+  // zero-row floor: (1e-14)^2 of the largest squared row norm at entry (the
+  // rows are shared out over the job's CTAs, one atomicMax per CTA on the
+  // order-preserving bits of a nonnegative double, then one barrier: every
+  // CTA reads the same value, so the result stays deterministic)
+  {
+    double mx = 0.0;
+    for (int i = cta * 8 + warp; i < J.nv; i += J.ctas * 8) {
+      const double* vi = J.v + (int64_t)i * J.ld;
+      double sq = 0.0;
+      for (int e = lane; e < J.len; e += 32) sq = fma(vi[e], vi[e], sq);
+      sq = warp_sum(sq);
+      mx = fmax(mx, sq);
+    }
+    if (lane == 0 && mx > 0.0)
+      atomicMax(J.gmax, (unsigned long long)__double_as_longlong(mx));
+    if (J.ctas > 1 && J.cluster) cluster_sync_all();
+    else if (J.ctas > 1) grid_barrier(J.bar, J.ctas, epoch);
+    else __syncthreads();
+  }
+  // (values-only jobs; with accumulated rotations the rows of zero singular
+  //  values must still come out mutually orthogonal for the vector outputs)
+  const double floor2 = J.acc ? 0.0 : 1e-28 * __longlong_as_double((long long)*reinterpret_cast<
+                                                  volatile unsigned long long*>(J.gmax));
   if (J.acc) {  // accumulated rotations start at the identity
     for (int64_t e = (int64_t)cta * kDenseThreads + tid; e < (int64_t)J.nv * J.nv;
          e += (int64_t)J.ctas * kDenseThreads) {
@@ -1041,7 +1071,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_bjacobi(BJacJob j0, BJacJob j
       for (int p = cta; p < npairs; p += J.ctas) {
         // (one block: nbe = 2 and its partner block is all padding)
         const int ba = rr_player(p, round, nbe), bb = rr_player(nbe - 1 - p, round, nbe);
-        rotated |= bj_pair(J, ba, bb, tol, dsm, &s_flag, inner_sweeps);
+        rotated |= bj_pair(J, ba, bb, tol, dsm, &s_flag, inner_sweeps, floor2);
       }
       if (J.ctas > 1) {
         if (J.cluster) cluster_sync_all();
@@ -1132,11 +1162,13 @@ int bjacobi_acc(double* v1, int64_t ld1, int nv1, int len1, double* sv1, int* ns
     c1 = cmax;
     if (c2 > 0) c2 = cmax;
   }
+  // per job: 64 bytes (barrier counter at 0, zero-row scale at 48) + sweep flags
   BJacJob a{v1, ld1, nv1, len1, sv1, nsv1, reinterpret_cast<unsigned*>(s),
-            reinterpret_cast<int*>(s + 64), 0, c1, clustered ? 1 : 0, acc1, ldacc1};
+            reinterpret_cast<int*>(s + 64), 0, c1, clustered ? 1 : 0, acc1, ldacc1,
+            reinterpret_cast<unsigned long long*>(s + 48)};
   BJacJob b{v2, ld2, nv2, len2, sv2, nsv2, reinterpret_cast<unsigned*>(s + 64 + kBjMaxSweeps * 4),
             reinterpret_cast<int*>(s + 128 + kBjMaxSweeps * 4), c1, c2, clustered ? 1 : 0,
-            nullptr, 0};
+            nullptr, 0, reinterpret_cast<unsigned long long*>(s + 64 + kBjMaxSweeps * 4 + 48)};
   int ms = kBjMaxSweeps;
   static const int inner = [] {  // RGSV_BJ_INNER: inner Jacobi sweeps per block pair
     const char* e = getenv("RGSV_BJ_INNER");

@@ -84,6 +84,12 @@ def stacked_extreme_singular_values(g1: "_dev.DevMatrix", g2: "_dev.DevMatrix"):
     r = stacked_r(g1, g2)
     if r is None:
         return 1.0, 0.0
+    # sigma_min <= min |R_jj| and sigma_max >= max |R_jj| for a triangular R:
+    # a diagonal ratio at or below the threshold already proves the deficiency
+    d = torch.diagonal(r[:n, :n]).abs()
+    dmax, dmin = float(d.max()), float(d.min())
+    if dmin <= 1e-12 * dmax:
+        return dmax, dmin
     rr = torch.zeros((n, n + (n & 1)), dtype=torch.float64, device="cuda")
     rr[:, :n].copy_(r[:n, :n])
     s = _jacobi_values(rr, n, n)

@@ -244,3 +244,71 @@ def test_random_core_factorizations():
             assert np.linalg.norm((sf.u * sf.s) @ sf.v.T - a) <= 1e-11 * np.linalg.norm(a), tag
             if rows >= cols:
                 assert abs(rg.pseudoinverse_norm(a) - 1.0 / s_ref[-1]) <= 1e-9 / s_ref[-1], tag
+
+
+def test_random_stacks_validation_verdict():
+    """GmpPair's stacked-rank check on random stacks (Gaussian, graded down to
+    1e-11, around the 1e-12 threshold, a duplicated or zero column; rows on
+    both sides of the Householder / CholeskyQR route boundary): the
+    reference's verdict sigma_min <= 1e-12 sigma_max from LAPACK's singular
+    values, RankDeficiencyError (never ConvergenceError: a zero column used
+    to stall the blocked Jacobi on R) and the cached norms."""
+    rng = np.random.default_rng(31)
+    for idx in range(36):
+        n = int(rng.integers(2, 500))
+        rows = int(rng.integers(n, 3000))
+        kind = str(rng.choice(["gauss", "graded", "dupcol", "zerocol", "borderline"]))
+        s = rng.standard_normal((rows, n))
+        if kind in ("graded", "borderline"):
+            u, _ = np.linalg.qr(s)
+            v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+            lo = rng.uniform(2, 11) if kind == "graded" else rng.uniform(11.3, 12.7)
+            s = (u * np.logspace(0, -float(lo), n)) @ v.T
+        elif kind == "dupcol" and n > 2:
+            s[:, -1] = s[:, 0] + s[:, 1]
+        elif kind == "zerocol":
+            s[:, int(rng.integers(0, n))] = 0.0
+        cut = int(rng.integers(1, rows))
+        tag = f"validate case {idx}: {kind} rows={rows} n={n} cut={cut}"
+        sv = np.linalg.svd(s, compute_uv=False)
+        ratio = sv[-1] / sv[0]
+        try:
+            pair = rg.GmpPair(s[:cut], s[cut:])
+            raised = False
+        except rg.RankDeficiencyError:
+            raised = True
+        if 3e-13 < ratio < 3e-12:  # within rounding of the threshold
+            continue
+        assert raised == (ratio <= 1e-12), (tag, ratio)
+        if not raised:
+            assert abs(pair.stack_norm2 - sv[0]) <= 1e-11 * sv[0], tag
+            assert abs(1.0 / pair.stack_pinv_norm - sv[-1]) \
+                <= max(0.02 * sv[-1], 1e-14 * sv[0]), tag
+
+
+def test_random_l_blocks_vs_oracle():
+    """engine.spectrum_from_l_blocks on random orthonormal-column stacks split
+    into L blocks, incl. blocks with exactly zero singular values (they used
+    to stall the blocked Jacobi): merged spectrum and counts vs the oracle
+    (4e-8: the sqrt(1 - x^2) completion near x = 1)."""
+    rng = np.random.default_rng(32)
+    for idx in range(36):
+        n = int(rng.integers(2, 300))
+        l1 = int(rng.integers(1, 400))
+        l2 = int(rng.integers(1, 400))
+        r = min(l1 + l2, n)
+        q, _ = np.linalg.qr(rng.standard_normal((l1 + l2, r)))
+        if rng.random() < 0.5 and r > 2:
+            q[:l1, : int(rng.integers(1, r))] = 0.0
+            q, _ = np.linalg.qr(q)
+        tag = f"seam case {idx}: l1={l1} l2={l2} n={n}"
+        try:
+            o = orc.spectrum_from_l_blocks(q[:l1], q[l1:], n, 1e-10)
+        except Exception:  # noqa: BLE001  (the reference's own invariant checks)
+            with pytest.raises(rg.GsvError):
+                rg.engine.spectrum_from_l_blocks(q[:l1], q[l1:], n, 1e-10)
+            continue
+        spec = rg.engine.spectrum_from_l_blocks(q[:l1], q[l1:], n, 1e-10)
+        assert (spec.r, spec.s) == (o[2], o[3]), tag
+        assert np.max(np.abs(spec.alphas - o[0])) <= 4e-8, tag
+        assert np.max(np.abs(spec.betas - o[1])) <= 4e-8, tag
