@@ -72,6 +72,21 @@ __device__ void jacobi_rows_body(JacobiJob J, int max_sweeps, int* __restrict__ 
   }
   const int nve = J.nv + (J.nv & 1);
   const double tol = fmax(1e-15, sqrt((double)J.len) * 2.220446049250313e-16);
+  // Zero-row floor: rows below 1e-14 of the largest row norm at entry are
+  // rounding noise of a rank-deficient input (re-injected by every rotation
+  // with a large row); they are neither rotated nor held against convergence.
+  for (int i = warp; i < J.nv; i += nwarps) {
+    const double* vi = J.v + (int64_t)i * J.ld;
+    double sq = 0.0;
+    for (int e = lane; e < J.len; e += 32) sq = fma(vi[e], vi[e], sq);
+    sq = warp_sum(sq);
+    if (lane == 0) nrm[i] = sq;
+  }
+  __syncthreads();
+  double gmax = 0.0;
+  for (int i = 0; i < J.nv; ++i) gmax = fmax(gmax, nrm[i]);
+  const double floor2 = 1e-28 * gmax;
+  __syncthreads();
   bool converged = (J.nv == 1);
   for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
     int rotated = 0;
@@ -91,7 +106,7 @@ __device__ void jacobi_rows_body(JacobiJob J, int max_sweeps, int* __restrict__ 
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+        if (ga != 0.0 && fmin(al, be) > floor2 && fabs(ga) > tol * sqrt(al * be)) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;

@@ -571,7 +571,14 @@ def run_host_batch(host_pairs, opts: GsvOptions, seeds=None) -> list:
     k1, k2 = widths
     plan = _dev.host_stream_plan(len(host_pairs), m, p, n, k1, k2)
     pks = plan.run(host_pairs, seeds, cfg.power_iters, opts.classify_tol)
-    return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]
+    runs = []
+    for hp, sd, pk, sub in zip(host_pairs, seeds, pks, plan.plans):
+        try:
+            runs.append(unpack(pk, sub, opts))
+        except RankDeficiencyError:  # sketch wider than the rank: see run_device_pipeline
+            runs.append(_general_run(GmpPair(hp[0], hp[1], check_rank=False), dataclasses.replace(
+                opts, extraction=dataclasses.replace(cfg, seed=sd))))
+    return runs
 
 
 _BATCH_SCAN: list = [None, None, None]  # [identity key, pairs (kept alive), result]
@@ -628,7 +635,14 @@ def run_device_batch(pairs, opts: GsvOptions, seeds=None) -> list:
         return _small_batch_runs(pairs, opts, seeds, k1)
     plan = _dev.batch_plan(len(pairs), first.m, first.p, first.n, k1, k2)
     pks = plan.run([(pr.g1, pr.g2) for pr in pairs], seeds, cfg.power_iters, opts.classify_tol)
-    return [unpack(pk, sub, opts) for pk, sub in zip(pks, plan.plans)]
+    runs = []
+    for pr, sd, pk, sub in zip(pairs, seeds, pks, plan.plans):
+        try:
+            runs.append(unpack(pk, sub, opts))
+        except RankDeficiencyError:  # sketch wider than the rank: see run_device_pipeline
+            runs.append(_general_run(pr, dataclasses.replace(
+                opts, extraction=dataclasses.replace(cfg, seed=sd))))
+    return runs
 
 
 class _PairMats:

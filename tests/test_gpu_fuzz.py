@@ -312,3 +312,52 @@ def test_random_l_blocks_vs_oracle():
         assert (spec.r, spec.s) == (o[2], o[3]), tag
         assert np.max(np.abs(spec.alphas - o[0])) <= 4e-8, tag
         assert np.max(np.abs(spec.betas - o[1])) <= 4e-8, tag
+
+
+def test_small_l_blocks_and_batches_with_zero_gsvs():
+    """The one-CTA Jacobi (< 64 vectors) on L blocks with exactly zero
+    singular values, and batched synth_gmp pairs (each matrix rank deficient,
+    sketch wider than its rank: the per-pair fallback of the batch path),
+    against the oracle."""
+    import torch
+
+    rng = np.random.default_rng(41)
+    for idx in range(40):
+        n = int(rng.integers(2, 60))
+        l1 = int(rng.integers(1, 64))
+        l2 = int(rng.integers(1, 64))
+        r = min(l1 + l2, n)
+        q, _ = np.linalg.qr(rng.standard_normal((l1 + l2, r)))
+        if rng.random() < 0.6 and r > 2:
+            q[:l1, : int(rng.integers(1, r))] = 0.0
+            q, _ = np.linalg.qr(q)
+        try:
+            o = orc.spectrum_from_l_blocks(q[:l1], q[l1:], n, 1e-10)
+        except Exception:  # noqa: BLE001
+            continue
+        spec = rg.engine.spectrum_from_l_blocks(q[:l1], q[l1:], n, 1e-10)
+        tag = f"small seam case {idx}: l1={l1} l2={l2} n={n}"
+        assert (spec.r, spec.s) == (o[2], o[3]), tag
+        assert np.max(np.abs(spec.alphas - o[0])) <= 4e-8, tag
+    for idx in range(8):
+        n = int(rng.integers(6, 33))
+        k = n // 2 + int(rng.integers(0, n - n // 2 + 1))
+        m = int(rng.integers(n + 5, 900))
+        p = int(rng.integers(n + 5, 900))
+        nb = int(rng.integers(1, 5))
+        hosts = []
+        for _ in range(nb):
+            res = rg.synth_gmp(rg.SynthSpec(m=m, p=p, n=n, rank_frac=float(rng.uniform(0.6, 1.0)),
+                                            seed=int(rng.integers(0, 999)), field="real"))
+            hosts.append((res.pair.g1.t.cpu().numpy().copy(), res.pair.g2.t.cpu().numpy().copy()))
+        seeds = [int(x) for x in rng.integers(0, 1000, nb)]
+        opts = rg.GsvOptions(extraction=rg.ExtractionConfig.fixed_rank(k, 0, 1))
+        pairs = [rg.GmpPair.resident(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+                 for a, b in hosts]
+        reps = rg.compare_batch(pairs, opts, seeds)
+        for j, (a, b) in enumerate(hosts):
+            o = orc.run_pipeline(a, b, k=k, q=1, seed=seeds[j])
+            sp = reps[j].spectrum
+            tag = f"zero-block batch case {idx}: n={n} k={k} m={m} p={p} pair {j}"
+            assert (sp.r, sp.s) == (o.r, o.s), tag
+            assert np.max(np.abs(sp.alphas - o.alphas)) <= 1e-6, tag
